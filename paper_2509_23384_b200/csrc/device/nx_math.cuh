@@ -1,0 +1,115 @@
+// Device math shared by every kernel: the perf model (Eq. 1-2), xoshiro256++,
+// warp helpers. Compiled with --fmad=false: the reference build has no FMA
+// contraction (proj/CMakeLists.txt:1-8, x86-64 baseline), so every a*b+c here
+// rounds twice exactly like the host code it replaces.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define NX_FULL 0xffffffffu
+
+namespace nxd {
+
+struct Params {  // PerfParams field order (proj/include/servesim/perf_model.h:14-27)
+  double tau0, w0, ws, tauB, tauS, p_max, kB, kS;
+};
+
+__device__ __forceinline__ Params params_from(const double* p) {
+  Params q;
+  q.tau0 = p[0]; q.w0 = p[1]; q.ws = p[2]; q.tauB = p[3];
+  q.tauS = p[4]; q.p_max = p[5]; q.kB = p[6]; q.kS = p[7];
+  return q;
+}
+__device__ __forceinline__ void params_to(const Params& q, double* p) {
+  p[0] = q.tau0; p[1] = q.w0; p[2] = q.ws; p[3] = q.tauB;
+  p[4] = q.tauS; p[5] = q.p_max; p[6] = q.kB; p[7] = q.kS;
+}
+__device__ __forceinline__ bool params_valid(const Params& p) {  // perf_model.cpp:33-36
+  return p.p_max > 0.0 && p.kB > 0.0 && p.kS > 0.0 && p.tau0 >= 0.0 && p.tauB >= 0.0 &&
+         p.tauS >= 0.0 && p.ws > 0.0 && p.w0 >= 0.0;
+}
+
+// nextafter(1.0, 0.0): saturation factors are clamped just below one
+// (perf_model.cpp:12-20).
+constexpr double kFactorMax = 0x1.fffffffffffffp-1;
+
+__device__ __forceinline__ double raw_factor(double k, double x) { return -expm1(-k * x); }
+__device__ __forceinline__ double clamp_factor(double f) { return f < kFactorMax ? f : kFactorMax; }
+__device__ __forceinline__ double sat(double k, double x) { return clamp_factor(raw_factor(k, x)); }
+
+// T(B,S) given the (clamped) batch factor fb — lets callers that sweep S at a
+// fixed B reuse fb; bitwise identical to predict_latency (perf_model.cpp:44-49).
+__device__ __forceinline__ double latency_fb(const Params& p, double fb, double b, double s) {
+  const double thr = p.p_max * fb * sat(p.kS, s);
+  const double work = p.w0 + p.ws * s;
+  return p.tau0 + work / thr + p.tauB * b + p.tauS * s;
+}
+__device__ __forceinline__ double predict(const Params& p, double b, double s) {
+  return latency_fb(p, sat(p.kB, b), b, s);
+}
+__device__ __forceinline__ double throughput(const Params& p, double b, double s) {
+  return p.p_max * sat(p.kB, b) * sat(p.kS, s);
+}
+
+__device__ __forceinline__ int64_t to_us(double ms) { return llround(ms * 1000.0); }
+__device__ __forceinline__ double to_ms(int64_t us) { return static_cast<double>(us) / 1000.0; }
+
+__device__ __forceinline__ uint64_t fnv1a(uint64_t h, uint64_t v) {  // sim.cpp:24-30
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    h ^= (v >> (8 * i)) & 0xff;
+    h *= 0x100000001b3ULL;
+  }
+  return h;
+}
+
+// xoshiro256++ (proj/include/servesim/rng.h:19-45)
+struct Rng {
+  uint64_t s[4];
+  __device__ __forceinline__ static uint64_t rotl(uint64_t v, int k) { return (v << k) | (v >> (64 - k)); }
+  __device__ __forceinline__ uint64_t next() {
+    const uint64_t out = rotl(s[0] + s[3], 23) + s[0];
+    const uint64_t t = s[1] << 17;
+    s[2] ^= s[0];
+    s[3] ^= s[1];
+    s[1] ^= s[2];
+    s[0] ^= s[3];
+    s[2] ^= t;
+    s[3] = rotl(s[3], 45);
+    return out;
+  }
+  __device__ __forceinline__ double uniform() {
+    return (static_cast<double>(next() >> 11) + 1.0) * 0x1.0p-53;
+  }
+  __device__ __forceinline__ double normal() {
+    const double u1 = uniform();
+    const double u2 = uniform();
+    return sqrt(-2.0 * log(u1)) * cos((2.0 * 3.141592653589793) * u2);
+  }
+};
+
+// ---- warp helpers -----------------------------------------------------------
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+__device__ __forceinline__ int warp_incl_scan(int v) {
+  const int lane = lane_id();
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int u = __shfl_up_sync(NX_FULL, v, o);
+    if (lane >= o) v += u;
+  }
+  return v;
+}
+
+// Fixed-order butterfly sum: every lane ends with the bitwise-same value
+// (each level adds commuting pairs), and the order never depends on timing.
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(NX_FULL, v, o);
+  return v;
+}
+__device__ __forceinline__ int warp_max_int(int v) {
+  return static_cast<int>(__reduce_max_sync(NX_FULL, static_cast<unsigned>(v)));
+}
+
+}  // namespace nxd

@@ -1,0 +1,78 @@
+// Per-warp replica state staged in shared memory + the execution context.
+//
+// One warp simulates one replica. Lane 0 is the "sequential" owner of every
+// shared scalar: all lanes run the same control flow and compute the same
+// values from shared state, but only lane 0 stores (`put`), bracketed by
+// __syncwarp so no lane reads a half-updated field. Lane-parallel sections
+// (scans over engines, candidate batches, learner samples) write only
+// lane-private slots and sync before anyone reads them.
+#pragma once
+#include "../nx_layout.h"
+#include "nx_math.cuh"
+
+namespace nxd {
+
+constexpr uint64_t kNoEvent = ~0ull;
+constexpr int kFbTable = 1024;  // batch-factor table entries per learner fit
+
+// Engine scalars (EngineSim + OnlineLearner + TradeoffEstimator + router view)
+struct EngSm {
+  Params lp;                                   // learner current_ (learner.h:90)
+  double alpha, beta, l_bar, td_min;           // TradeoffModel (lens.h:22-27)
+  double plan_pred, plan_target, actual, learn_y;
+  double lat_sum;
+  double rep_lhat, rep_wload, rep_mfree, rep_pmax, rep_at;  // router's report copy
+  uint64_t rng[4];
+  uint64_t step_t, learn_t, report_t;          // pending-event slots (kNoEvent = none)
+  int64_t started_us, seen, rep_qlen, tw_degen;
+  int64_t cnt[7];                              // LearnerCounters
+  uint32_t step_seq, learn_seq, report_seq;
+  int32_t wq_head, wq_len, rq_len;
+  int32_t pinned, reserved, cache_blocks, lru_head, lru_tail;
+  int32_t busy, plan_n, plan_b, plan_s, plan_wspan, plan_overload;
+  int32_t learn_b, learn_s;
+  int32_t ring_size, ring_head, tw_head, tw_len, dq_head, dq_len, lat_head, lat_len;
+  int32_t has_rep;
+};
+
+struct RepSm {
+  uint64_t ev_hash, rr_next, rng[4];
+  int64_t arrived, rejected, pending, n_rec, events, info;
+  double l_bar_ema;
+  uint32_t next_seq;
+  int32_t cursor, status, site;
+};
+
+struct Ctx {
+  const NxPools* P;
+  const NxReplicaDesc* d;
+  const NxEngineDesc* ed;  // this replica's engines
+  RepSm* rs;
+  EngSm* eng;
+  int32_t* prefix;         // LENS prefix sums (union with chunk)
+  double* chunk;           // 32 x 5 staging rows for exact-order folds
+  double* scratch;         // learner scratch in HBM (fs cache, fb table, rows)
+  int64_t roff, soff;
+  int n_eng, n_req, n_sess, lane, prefix_cap;
+};
+
+template <class T>
+__device__ __forceinline__ void put(T& dst, T v) {
+  __syncwarp();
+  if (lane_id() == 0) dst = v;
+  __syncwarp();
+}
+
+// Raise a reference exception: first error wins, replica stops.
+__device__ __forceinline__ void fail(Ctx& c, int status, int site, int64_t info) {
+  __syncwarp();
+  if (c.lane == 0 && c.rs->status == 0) {
+    c.rs->status = status;
+    c.rs->site = site;
+    c.rs->info = info;
+  }
+  __syncwarp();
+}
+__device__ __forceinline__ bool failed(const Ctx& c) { return c.rs->status != 0; }
+
+}  // namespace nxd

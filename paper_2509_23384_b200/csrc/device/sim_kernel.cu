@@ -1,0 +1,1132 @@
+// K5 — batched lockstep discrete-event simulation, one warp per replica.
+//
+// Each warp runs one servesim::Simulation (proj/src/sim.cpp:245-347) to
+// completion. The reference's std::priority_queue<SimEvent> is replaced by
+// per-engine event slots (step completion, learner update, state report,
+// report-delivery FIFO head) plus an arrival cursor; the next event is a
+// warp-wide (time_us, sequence) minimum, so the processing order — and hence
+// the FNV event hash — equals the reference's. Inside an event the warp's
+// lanes parallelise over engines (K3 PRISM scorer), candidate batch sizes
+// (K2 LENS budget search), allocations (step completion) and learner samples
+// (K4 refit, nx_learner.cuh).
+#include "nx_learner.cuh"
+
+namespace nxd {
+
+constexpr double kInf = __builtin_huge_val();
+
+// ---- small helpers ------------------------------------------------------------
+__device__ __forceinline__ int blocks_for(int tokens, int block) { return (tokens + block - 1) / block; }
+__device__ __forceinline__ int remaining(const Ctx& c, int r) {
+  return c.P->prompt[c.roff + r] - c.P->prefilled[c.roff + r];
+}
+
+// target_latency (lens.cpp:10-31)
+__device__ double target_latency(const Ctx& c, const EngSm& g, int wait_count) {
+  const NxReplicaDesc& d = *c.d;
+  const double td_tpot = d.tpot_slo;
+  const double td_ttft = (g.alpha - d.ttft_slo) / g.beta;
+  double t;
+  if (g.l_bar > g.beta) {
+    const double lo = (g.td_min < td_ttft) ? td_ttft : g.td_min;  // max(td_min, td_ttft)
+    t = (lo < td_tpot) ? lo : td_tpot;                              // min(td_tpot, .)
+  } else {
+    t = td_tpot;
+  }
+  if (wait_count > 0) {
+    const double q = static_cast<double>(wait_count) / d.q_ref;
+    const double relax = (q < 1.0) ? q : 1.0;
+    t += relax * (td_tpot - t);
+  }
+  return t;
+}
+
+// Inclusive prefix sums of the remaining prompts of the first `count` waiters
+// into c.prefix[0..count] (prefix[0] = 0). lens.cpp:121-124.
+__device__ void build_prefix(Ctx& c, const int32_t* wq, int count) {
+  __syncwarp();
+  if (c.lane == 0) c.prefix[0] = 0;
+  int carry = 0;
+  for (int base = 0; base < count; base += 32) {
+    const int i = base + c.lane;
+    const int v = i < count ? remaining(c, wq[i]) : 0;
+    const int s = warp_incl_scan(v);
+    if (i < count) c.prefix[i + 1] = carry + s;
+    carry += __shfl_sync(NX_FULL, s, 31);
+  }
+  __syncwarp();
+}
+
+// first j in [0, hi] with prefix[j] >= need (prefix strictly increasing)
+__device__ __forceinline__ int lower_bound_prefix(const int32_t* pre, int hi, int need) {
+  int lo = 0;
+  while (lo < hi) {
+    const int m = (lo + hi) >> 1;
+    if (pre[m] >= need) hi = m;
+    else lo = m + 1;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ void set_plan(Ctx& c, EngSm& g, int n, int b, int s, double pred,
+                                         double target, int wspan, int overload) {
+  __syncwarp();
+  if (c.lane == 0) {
+    g.plan_n = n;
+    g.plan_b = b;
+    g.plan_s = s;
+    g.plan_pred = pred;
+    g.plan_target = target;
+    g.plan_wspan = wspan;
+    g.plan_overload = overload;
+  }
+  __syncwarp();
+}
+
+// Writes the run-queue decodes [0, R) of a plan.
+__device__ __forceinline__ void write_decodes(Ctx& c, const int32_t* rq, int R, int32_t* preq,
+                                              int32_t* ptok) {
+  for (int i = c.lane; i < R; i += 32) {
+    preq[i] = rq[i];
+    ptok[i] = -1;
+  }
+}
+
+// ---- K2: LENS schedule_step (lens.cpp:96-146) -----------------------------------
+__device__ void plan_lens(Ctx& c, int e) {
+  EngSm& g = c.eng[e];
+  const NxEngineDesc& ed = c.ed[e];
+  const int R = g.rq_len, W = g.wq_len, qmax = ed.q_max, mmax = ed.m_max;
+  const int32_t* wq = c.P->wq + ed.wq_off + g.wq_head;
+  const int32_t* rq = c.P->rq + ed.rq_off;
+  int32_t* preq = c.P->plan_req + ed.plan_off;
+  int32_t* ptok = c.P->plan_tok + ed.plan_off;
+  const Params P = g.lp;
+  const double target = target_latency(c, g, W);
+  if (R > qmax) {  // transient overload: truncated decode plan (lens.cpp:108-117)
+    write_decodes(c, rq, qmax, preq, ptok);
+    set_plan(c, g, qmax, qmax, qmax, predict(P, qmax, qmax), target, 0, 1);
+    return;
+  }
+  if (!(target > 0.0)) {  // binary_search_budget precondition (lens.cpp:36-38)
+    fail(c, 1, NX_SITE_BISECT, 0);
+    return;
+  }
+  const int b_lo = R > 1 ? R : 1;
+  const int b_hi = (R + W < qmax) ? R + W : qmax;
+  const int span = b_hi - R;
+  build_prefix(c, wq, span);
+  const int32_t* pre = c.prefix;
+  const double thr_eps = target * c.d->eps_ratio;
+  const int iters = c.d->n_iters;
+  double best_err = kInf;
+  int best_budget = -1;
+  for (int B0 = b_lo; B0 <= b_hi; B0 += 32) {
+    const int B = B0 + c.lane;
+    const bool act = B <= b_hi;
+    double err = kInf;
+    int budget = 0;
+    if (act) {
+      const int avail = R + pre[B - R];
+      int s_cap = (mmax < avail) ? mmax : avail;
+      s_cap = (B < s_cap) ? s_cap : B;  // max(b, min(s_cap, m_max))
+      const double bd = static_cast<double>(B);
+      const double fb = sat(P.kB, bd);
+      int lo = B, hi = s_cap;
+      budget = B;
+      for (int it = 0; it < iters; ++it) {  // binary_search_budget (lens.cpp:46-58)
+        if (lo > hi) break;
+        const int mid = (lo + hi) / 2;
+        if (latency_fb(P, fb, bd, static_cast<double>(mid)) <= target) {
+          budget = mid;
+          lo = mid + 1;
+        } else {
+          hi = mid - 1;
+        }
+      }
+      // realize(allocate_tokens(...)): S = budget, b = R + first j with prefix[j] >= budget - R
+      const int j = lower_bound_prefix(pre, B - R, budget - R);
+      err = fabs(predict(P, static_cast<double>(R + j), static_cast<double>(budget)) - target);
+    }
+    // first B whose error is below eps*target ends the sweep (the sequential
+    // loop's early exit fires exactly there); otherwise keep the first strict min
+    const unsigned hit = __ballot_sync(NX_FULL, act && err < thr_eps);
+    if (hit) {
+      best_budget = __shfl_sync(NX_FULL, budget, __ffs(hit) - 1);
+      break;
+    }
+    double v = (act && !isnan(err)) ? err : kInf;
+    int who = c.lane;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(NX_FULL, v, o);
+      const int ow = __shfl_xor_sync(NX_FULL, who, o);
+      if (ov < v || (ov == v && ow < who)) {
+        v = ov;
+        who = ow;
+      }
+    }
+    if (v < best_err) {
+      best_err = v;
+      best_budget = __shfl_sync(NX_FULL, budget, who);
+    }
+  }
+  if (best_budget < 0) {  // every candidate error was NaN: empty plan
+    set_plan(c, g, 0, 0, 0, 0.0, target, 0, 0);
+    return;
+  }
+  const int need = best_budget - R;
+  const int j = lower_bound_prefix(pre, span, need);
+  write_decodes(c, rq, R, preq, ptok);
+  for (int k = c.lane; k < j; k += 32) {  // allocate_tokens waiters (lens.cpp:71-77)
+    const int rem = pre[k + 1] - pre[k];
+    const int left = need - pre[k];
+    preq[R + k] = wq[k];
+    ptok[R + k] = rem < left ? rem : left;
+  }
+  set_plan(c, g, R + j, R + j, best_budget,
+           predict(P, static_cast<double>(R + j), static_cast<double>(best_budget)), target, j, 0);
+}
+
+// ---- baseline engine policies (engine.cpp:61-108) -------------------------------
+__device__ void plan_baseline(Ctx& c, int e) {
+  EngSm& g = c.eng[e];
+  const NxEngineDesc& ed = c.ed[e];
+  const int R = g.rq_len, W = g.wq_len, qmax = ed.q_max, mmax = ed.m_max;
+  const int32_t* wq = c.P->wq + ed.wq_off + g.wq_head;
+  const int32_t* rq = c.P->rq + ed.rq_off;
+  int32_t* preq = c.P->plan_req + ed.plan_off;
+  int32_t* ptok = c.P->plan_tok + ed.plan_off;
+  const Params P = g.lp;
+  if (ed.policy == 1) {  // prefill_priority
+    if (W > 0) {
+      const int cnt = W < qmax ? W : qmax;
+      build_prefix(c, wq, cnt);
+      int j = 0;  // whole prompts while they fit under m_max
+      for (int base = 0; base < cnt; base += 32) {
+        const int k = base + c.lane;
+        const unsigned ok = __ballot_sync(NX_FULL, k < cnt && c.prefix[k + 1] <= mmax);
+        j += __popc(ok);
+        if (ok != NX_FULL) break;
+      }
+      if (j == 0) {
+        fail(c, 2, NX_SITE_PREFILL_CAP, ed.engine_id);
+        return;
+      }
+      for (int k = c.lane; k < j; k += 32) {
+        preq[k] = wq[k];
+        ptok[k] = c.prefix[k + 1] - c.prefix[k];
+      }
+      const int s = c.prefix[j];
+      set_plan(c, g, j, j, s, predict(P, j, s), 0.0, j, 0);
+    } else {
+      write_decodes(c, rq, R, preq, ptok);
+      set_plan(c, g, R, R, R, predict(P, R, R), 0.0, 0, 0);
+    }
+    return;
+  }
+  // static_chunked: allocate_tokens against a fixed budget
+  const int b = (R + W < qmax) ? R + W : qmax;
+  const int sb = (ed.static_budget < b) ? b : ed.static_budget;
+  const int s = (mmax < sb) ? mmax : sb;
+  if (b < R || s < b) {
+    fail(c, 1, NX_SITE_ALLOCATE, b);
+    return;
+  }
+  const int slots = b - R;
+  const int budget = s - R;
+  build_prefix(c, wq, slots);
+  const int j = budget > 0 ? lower_bound_prefix(c.prefix, slots, budget) : 0;
+  const int jj = j;  // waiters k < slots with prefix[k] < budget
+  write_decodes(c, rq, R, preq, ptok);
+  int part = 0;
+  for (int k = c.lane; k < jj; k += 32) {
+    const int rem = c.prefix[k + 1] - c.prefix[k];
+    const int left = budget - c.prefix[k];
+    const int take = rem < left ? rem : left;
+    preq[R + k] = wq[k];
+    ptok[R + k] = take;
+    part += take;
+  }
+  const int stot = R + static_cast<int>(__reduce_add_sync(NX_FULL, static_cast<unsigned>(part)));
+  const int n = R + jj;
+  set_plan(c, g, n, n, stot, n > 0 ? predict(P, n, stot) : 0.0, 0.0, jj, 0);
+}
+
+// ---- trim_for_kv (engine.cpp:184-214) ----------------------------------------------
+__device__ void trim_for_kv(Ctx& c, int e) {
+  EngSm& g = c.eng[e];
+  const NxEngineDesc& ed = c.ed[e];
+  int32_t* preq = c.P->plan_req + ed.plan_off;
+  int32_t* ptok = c.P->plan_tok + ed.plan_off;
+  const int n = g.plan_n;
+  __syncwarp();
+  if (c.lane == 0) {
+    int kept = 0;
+    bool trimmed = false;
+    for (int k = 0; k < n; ++k) {
+      const int r = preq[k];
+      const int tok = ptok[k];
+      bool keep;
+      if (tok < 0 || c.P->kv_admitted[c.roff + r]) {
+        keep = true;
+      } else if (trimmed) {
+        keep = false;
+      } else {
+        const int foot = blocks_for(c.P->prompt[c.roff + r] + c.P->target[c.roff + r], ed.block_size);
+        const int fut = foot - blocks_for(c.P->prefilled[c.roff + r] + c.P->decoded[c.roff + r],
+                                          ed.block_size);
+        if (static_cast<int64_t>(g.pinned) + g.reserved + fut <= ed.kv_blocks) {
+          g.reserved += fut;
+          c.P->kv_admitted[c.roff + r] = 1;
+          keep = true;
+        } else {
+          trimmed = true;
+          keep = false;
+        }
+      }
+      if (keep) {
+        preq[kept] = r;
+        ptok[kept] = tok;
+        ++kept;
+      }
+    }
+    if (kept != n) {
+      int s = 0;
+      for (int k = 0; k < kept; ++k) s += ptok[k] < 0 ? 1 : ptok[k];
+      g.plan_n = kept;
+      g.plan_b = kept;
+      g.plan_s = s;
+      g.plan_pred = kept > 0 ? predict(g.lp, kept, s) : 0.0;
+    }
+  }
+  __syncwarp();
+}
+
+// ---- begin_step (engine.cpp:216-228) + step event (sim.cpp:143-166) ----------------
+__device__ void try_begin_step(Ctx& c, int e, int64_t now_us) {
+  EngSm& g = c.eng[e];
+  __syncwarp();
+  if (g.busy || (g.wq_len == 0 && g.rq_len == 0)) return;
+  const NxEngineDesc& ed = c.ed[e];
+  if (ed.policy == 0) plan_lens(c, e);
+  else plan_baseline(c, e);
+  if (failed(c) || g.plan_n == 0) return;
+  trim_for_kv(c, e);
+  if (g.plan_n == 0) return;
+  __syncwarp();
+  if (c.lane == 0) {
+    const Params tp = params_from(ed.tp);
+    double actual = predict(tp, g.plan_b, g.plan_s);  // oracle_latency (engine.cpp:128-132)
+    if (ed.noise_sigma != 0.0) {
+      Rng rng;
+      for (int i = 0; i < 4; ++i) rng.s[i] = g.rng[i];
+      actual = actual * exp(ed.noise_sigma * rng.normal());
+      for (int i = 0; i < 4; ++i) g.rng[i] = rng.s[i];
+    }
+    const int64_t d = to_us(actual);
+    g.busy = 1;
+    g.started_us = now_us;
+    g.actual = actual;
+    g.step_t = static_cast<uint64_t>(now_us + (d > 1 ? d : 1));
+    g.step_seq = c.rs->next_seq++;
+  }
+  __syncwarp();
+}
+
+// ---- prefix cache LRU (engine.cpp:284-305), lane 0 only ----------------------------
+struct Lru {
+  int32_t* tok;
+  int32_t* prev;
+  int32_t* next;
+};
+__device__ __forceinline__ Lru lru_of(const Ctx& c, int e) {
+  const int64_t off = c.ed[e].cache_off;
+  return {c.P->c_tokens + off, c.P->c_prev + off, c.P->c_next + off};
+}
+__device__ __forceinline__ void lru_unlink(EngSm& g, const Lru& L, int s) {
+  const int p = L.prev[s], n = L.next[s];
+  if (p >= 0) L.next[p] = n;
+  else g.lru_head = n;
+  if (n >= 0) L.prev[n] = p;
+  else g.lru_tail = p;
+  L.tok[s] = -1;
+}
+__device__ __forceinline__ void evict_to_fit(EngSm& g, const Lru& L, int kv_blocks, int pinned,
+                                             int block) {
+  while (g.cache_blocks > kv_blocks - pinned && g.lru_head >= 0) {
+    const int v = g.lru_head;
+    g.cache_blocks -= blocks_for(L.tok[v], block);
+    lru_unlink(g, L, v);
+  }
+}
+__device__ __forceinline__ void cache_insert(EngSm& g, const Lru& L, int s, int tokens,
+                                             int kv_blocks, int pinned, int block) {
+  if (L.tok[s] >= 0) {
+    g.cache_blocks -= blocks_for(L.tok[s], block);
+    lru_unlink(g, L, s);
+  }
+  L.tok[s] = tokens;
+  L.prev[s] = g.lru_tail;
+  L.next[s] = -1;
+  if (g.lru_tail >= 0) L.next[g.lru_tail] = s;
+  else g.lru_head = s;
+  g.lru_tail = s;
+  g.cache_blocks += blocks_for(tokens, block);
+  evict_to_fit(g, L, kv_blocks, pinned, block);
+}
+
+// ---- admit (engine.cpp:139-169), lane 0 only ---------------------------------------
+__device__ bool admit(Ctx& c, int e, int r) {
+  EngSm& g = c.eng[e];
+  const NxEngineDesc& ed = c.ed[e];
+  if (ed.wait_cap > 0 && g.wq_len >= ed.wait_cap) return false;
+  const Lru L = lru_of(c, e);
+  const int sess = c.P->session[c.roff + r];
+  const int cached = L.tok[sess];
+  if (cached >= 0) {
+    const int prompt = c.P->prompt[c.roff + r];
+    const int credit = cached < prompt - 1 ? cached : prompt - 1;
+    const int cb = blocks_for(credit, ed.block_size);
+    if (credit > 0 && static_cast<int64_t>(g.pinned) + g.reserved + cb <= ed.kv_blocks) {
+      g.cache_blocks -= blocks_for(cached, ed.block_size);
+      lru_unlink(g, L, sess);
+      c.P->prefilled[c.roff + r] = credit;
+      g.pinned += cb;
+    }
+  }
+  c.P->wq[ed.wq_off + g.wq_head + g.wq_len] = r;
+  g.wq_len += 1;
+  c.P->req_engine[c.roff + r] = e;
+  return true;
+}
+
+// ---- TradeoffEstimator refit (lens.cpp:161-188), exact left folds --------------------
+__device__ void tradeoff_refit(Ctx& c, int e) {
+  EngSm& g = c.eng[e];
+  const NxEngineDesc& ed = c.ed[e];
+  const int n = g.tw_len;
+  if (n < 2) return;
+  const double* tp = c.P->tw_ttft + ed.tw_off;
+  const double* td = c.P->tw_tpot + ed.tw_off;
+  const int head = g.tw_head;
+  // lane 0 folds ttft, lane 1 folds tpot (window order: oldest first)
+  double m = 0.0;
+  if (c.lane < 2) {
+    const double* src = c.lane == 0 ? tp : td;
+    for (int i = 0; i < n; ++i) m += src[(head + i) % NX_TW_CAP];
+  }
+  const double dn = static_cast<double>(n);
+  const double mtp = __shfl_sync(NX_FULL, m, 0) / dn;
+  const double mtd = __shfl_sync(NX_FULL, m, 1) / dn;
+  double acc = 0.0;  // lane 0: var, lane 1: cov
+  if (c.lane < 2) {
+    for (int i = 0; i < n; ++i) {
+      const int k = (head + i) % NX_TW_CAP;
+      const double dd = td[k] - mtd;
+      acc += c.lane == 0 ? dd * dd : dd * (tp[k] - mtp);
+    }
+  }
+  const double var = __shfl_sync(NX_FULL, acc, 0);
+  const double cov = __shfl_sync(NX_FULL, acc, 1);
+  const double sd = sqrt(var / dn);
+  __syncwarp();
+  if (c.lane == 0) {
+    if (sd <= 0.15 * mtd) {
+      g.tw_degen += 1;
+    } else {
+      const double slope = cov / var;
+      const double nb = -slope;
+      g.beta = (1e-3 < nb) ? nb : 1e-3;
+      g.alpha = mtp + g.beta * mtd;
+    }
+  }
+  __syncwarp();
+}
+
+// ---- complete_step (engine.cpp:230-282) + handle_step_complete (sim.cpp:196-224) ----
+__device__ void step_complete(Ctx& c, int e, int64_t now_us) {
+  EngSm& g = c.eng[e];
+  const NxEngineDesc& ed = c.ed[e];
+  const NxPools& P = *c.P;
+  const int64_t ro = c.roff;
+  const int n = g.plan_n, block = ed.block_size;
+  const int32_t* preq = P.plan_req + ed.plan_off;
+  const int32_t* ptok = P.plan_tok + ed.plan_off;
+  const double now = to_ms(now_us);
+  const Lru L = lru_of(c, e);
+  int* st_sess = reinterpret_cast<int*>(c.chunk);  // per-chunk staging for lane 0
+  int* st_tok = st_sess + 32;
+  int* st_pin = st_sess + 64;
+  int* st_req = st_sess + 96;
+  int pinned = g.pinned;
+  int dsum = 0, n_fin = 0, n_first = 0;
+  put(g.busy, 0);
+  for (int base = 0; base < n; base += 32) {
+    const int k = base + c.lane;
+    int delta = 0, held = 0, r = -1, tokens = 0;
+    bool first = false, fin = false;
+    if (k < n) {
+      r = preq[k];
+      const int tok = ptok[k];
+      int pre = P.prefilled[ro + r], dec = P.decoded[ro + r];
+      const int before = blocks_for(pre + dec, block);
+      if (tok >= 0) pre += tok;
+      else dec += 1;
+      const int after = blocks_for(pre + dec, block);
+      delta = after - before;
+      P.prefilled[ro + r] = pre;
+      P.decoded[ro + r] = dec;
+      first = tok >= 0 && pre == P.prompt[ro + r];
+      fin = tok < 0 && dec == P.target[ro + r];
+      if (first) P.first_us[ro + r] = now_us;
+      if (fin) {
+        held = after;
+        tokens = pre + dec;
+      }
+    }
+    // pinned as seen by cache_insert of allocation k (after its own release)
+    const int adj = delta - held;
+    const int scan = warp_incl_scan(adj);
+    const int pin_k = pinned + scan;
+    pinned += __shfl_sync(NX_FULL, scan, 31);
+    dsum += static_cast<int>(__reduce_add_sync(NX_FULL, static_cast<unsigned>(delta)));
+    const unsigned finm = __ballot_sync(NX_FULL, fin);
+    n_first += __popc(__ballot_sync(NX_FULL, first));
+    if (finm) {
+      __syncwarp();
+      if (fin) {
+        st_sess[c.lane] = P.session[ro + r];
+        st_tok[c.lane] = tokens;
+        st_pin[c.lane] = pin_k;
+        st_req[c.lane] = r;
+      }
+      __syncwarp();
+      if (c.lane == 0) {
+        unsigned m = finm;
+        while (m) {
+          const int l = __ffs(m) - 1;
+          m &= m - 1;
+          const int rr = st_req[l];
+          cache_insert(g, L, st_sess[l], st_tok[l], ed.kv_blocks, st_pin[l], block);
+          // CompletionStats + TradeoffEstimator EMA/window (lens.cpp:149-160)
+          const int tgt = P.target[ro + rr];
+          const double first_ms = to_ms(P.first_us[ro + rr]);
+          const double ttft = first_ms - P.arr_ms[ro + rr];
+          const double tpot = tgt >= 2 ? (now - first_ms) / static_cast<double>(tgt - 1) : 0.0;
+          const double lb = g.l_bar + 0.05 * (static_cast<double>(tgt) - g.l_bar);
+          g.l_bar = (1.0 < lb) ? lb : 1.0;
+          if (tgt >= 2) {
+            int slot;
+            if (g.tw_len < NX_TW_CAP) {
+              slot = (g.tw_head + g.tw_len) % NX_TW_CAP;
+              g.tw_len += 1;
+            } else {
+              slot = g.tw_head;
+              g.tw_head = (g.tw_head + 1) % NX_TW_CAP;
+            }
+            P.tw_ttft[ed.tw_off + slot] = ttft;
+            P.tw_tpot[ed.tw_off + slot] = tpot;
+          }
+          // RequestRecord + Router::on_completion (router.cpp:83-92)
+          P.done_us[ro + rr] = now_us;
+          P.records[ro + c.rs->n_rec] = rr;
+          c.rs->n_rec += 1;
+          if (c.d->route_policy == 4) {
+            if (g.lat_len >= ed.lat_cap) {
+              c.rs->status = 1;
+              c.rs->site = NX_SITE_OVERFLOW;
+            } else {
+              const int slot = (g.lat_head + g.lat_len) % ed.lat_cap;
+              P.lat_t[ed.lat_off + slot] = now;
+              P.lat_e2e[ed.lat_off + slot] = now - P.arr_ms[ro + rr];
+              g.lat_len += 1;
+              g.lat_sum += now - P.arr_ms[ro + rr];
+            }
+          }
+          const double le = c.rs->l_bar_ema + 0.05 * (static_cast<double>(tgt) - c.rs->l_bar_ema);
+          c.rs->l_bar_ema = le < 1.0 ? 1.0 : le;
+          P.sess_engine[c.soff + P.session[ro + rr]] = e;
+        }
+      }
+      __syncwarp();
+    }
+    n_fin += __popc(finm);
+  }
+  __syncwarp();
+  if (c.lane == 0) {
+    g.pinned = pinned;
+    g.reserved -= dsum;
+    evict_to_fit(g, L, ed.kv_blocks, pinned, block);
+  }
+  __syncwarp();
+  // run queue: drop finished (stable), then append new runners in plan order
+  int32_t* rq = P.rq + ed.rq_off;
+  int out = g.rq_len;
+  if (n_fin) {
+    out = 0;
+    const int len = g.rq_len;
+    for (int base = 0; base < len; base += 32) {
+      const int i = base + c.lane;
+      const int r = i < len ? rq[i] : 0;
+      const bool keep = i < len && P.decoded[ro + r] != P.target[ro + r];
+      const unsigned m = __ballot_sync(NX_FULL, keep);
+      __syncwarp();
+      if (keep) rq[out + __popc(m & ((1u << c.lane) - 1))] = r;
+      out += __popc(m);
+      __syncwarp();
+    }
+  }
+  if (n_first) {
+    int32_t* wq = P.wq + ed.wq_off;
+    for (int base = 0; base < n; base += 32) {
+      const int k = base + c.lane;
+      bool nr = false;
+      int r = 0;
+      if (k < n && ptok[k] >= 0) {
+        r = preq[k];
+        nr = P.prefilled[ro + r] == P.prompt[ro + r];
+      }
+      const unsigned m = __ballot_sync(NX_FULL, nr);
+      if (nr) rq[out + __popc(m & ((1u << c.lane) - 1))] = r;
+      out += __popc(m);
+    }
+    __syncwarp();
+    // wait queue: drop prefill-complete requests from the scheduled window,
+    // keeping survivors in FCFS order at the window's tail
+    if (c.lane == 0) {
+      const int head = g.wq_head, span = g.plan_wspan;
+      int wpos = head + span - 1;
+      for (int i = span - 1; i >= 0; --i) {
+        const int r = wq[head + i];
+        if (P.prefilled[ro + r] != P.prompt[ro + r]) wq[wpos--] = r;
+      }
+      const int removed = wpos + 1 - head;
+      g.wq_head = head + removed;
+      g.wq_len -= removed;
+    }
+  }
+  __syncwarp();
+  if (c.lane == 0) {
+    g.rq_len = out;
+    // learner update event at the same timestamp (sim.cpp:216-221)
+    g.learn_t = static_cast<uint64_t>(now_us);
+    g.learn_seq = c.rs->next_seq++;
+    g.learn_b = g.plan_b;
+    g.learn_s = g.plan_s;
+    g.learn_y = g.actual;
+  }
+  __syncwarp();
+  if (n_fin) tradeoff_refit(c, e);
+  try_begin_step(c, e, now_us);
+}
+
+// ---- state report (sim.cpp:226-243, engine.cpp:307-332), lane 0 only -----------
+__device__ void state_report(Ctx& c, int e, int64_t now_us) {
+  EngSm& g = c.eng[e];
+  const NxEngineDesc& ed = c.ed[e];
+  __syncwarp();
+  if (c.lane == 0) {
+    const double now = to_ms(now_us);
+    double l_hat = 0.0;
+    if (g.busy) {
+      const double v = g.plan_pred - (now - to_ms(g.started_us));
+      l_hat = (0.0 < v) ? v : 0.0;
+    }
+    double pending = 0.0, demand = 0.0;
+    const int32_t* wq = c.P->wq + ed.wq_off + g.wq_head;
+    for (int i = 0; i < g.wq_len; ++i) {
+      const double rem = static_cast<double>(remaining(c, wq[i]));
+      pending += rem;
+      demand += rem + g.l_bar;
+    }
+    const int64_t q = static_cast<int64_t>(g.wq_len) + g.rq_len;
+    const double w_load = pending + 32.0 * static_cast<double>(q);
+    const double free_tok = static_cast<double>(static_cast<int64_t>(ed.kv_blocks - g.pinned) *
+                                                static_cast<int64_t>(ed.block_size));
+    const double mf = free_tok - demand;
+    if (g.dq_len >= ed.dq_cap) {
+      c.rs->status = 1;
+      c.rs->site = NX_SITE_OVERFLOW;
+    } else {
+      const int slot = (g.dq_head + g.dq_len) % ed.dq_cap;
+      const int64_t o = ed.dq_off + slot;
+      c.P->dq_t[o] = now_us + ed.stale_us;
+      c.P->dq_seq[o] = c.rs->next_seq++;
+      double* sv = c.P->dq_sv + 5 * o;
+      sv[0] = l_hat;
+      sv[1] = w_load;
+      sv[2] = (0.0 < mf) ? mf : 0.0;
+      sv[3] = g.lp.p_max;
+      sv[4] = now;
+      c.P->dq_qlen[o] = q;
+      g.dq_len += 1;
+    }
+    g.report_t = static_cast<uint64_t>(now_us + ed.period_us);
+    g.report_seq = c.rs->next_seq++;
+  }
+  __syncwarp();
+}
+
+// ---- K3: Router::route (router.cpp:141-289) ------------------------------------
+__device__ __forceinline__ double score_load(double w_load, double p_max, double half) {
+  const double rho = w_load / p_max;
+  return 1.0 / (1.0 + rho / half);
+}
+
+// lexicographic first minimum of (key, lane) over lanes with valid keys
+__device__ __forceinline__ int warp_argmin_i64(int64_t key, bool valid) {
+  int64_t v = valid ? key : INT64_MAX;
+  int who = valid ? lane_id() : 64;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const int64_t ov = __shfl_xor_sync(NX_FULL, v, o);
+    const int ow = __shfl_xor_sync(NX_FULL, who, o);
+    if (ov < v || (ov == v && ow < who)) {
+      v = ov;
+      who = ow;
+    }
+  }
+  return who;
+}
+
+__device__ int least_loaded(Ctx& c) {
+  const int e = c.lane;
+  const bool on = e < c.n_eng;
+  int64_t len = 0;
+  if (on && c.eng[e].has_rep) len = c.eng[e].rep_qlen;
+  return warp_argmin_i64(len, on);
+}
+
+__device__ int route(Ctx& c, int rid, double now) {
+  const NxReplicaDesc& d = *c.d;
+  const int n = c.n_eng;
+  const int sess = c.P->session[c.roff + rid];
+  int32_t* sess_eng = c.P->sess_engine + c.soff;
+  int chosen = 0;
+  __syncwarp();
+  switch (d.route_policy) {
+    case 1: {  // round_robin
+      chosen = static_cast<int>(c.rs->rr_next % static_cast<uint64_t>(n));
+      put(c.rs->rr_next, c.rs->rr_next + 1);
+      break;
+    }
+    case 2: {  // session_affinity
+      const int se = sess_eng[sess];
+      if (se >= 0) {
+        chosen = se;
+      } else {
+        chosen = static_cast<int>(c.rs->rr_next % static_cast<uint64_t>(n));
+        put(c.rs->rr_next, c.rs->rr_next + 1);
+      }
+      break;
+    }
+    case 3:
+      chosen = least_loaded(c);
+      break;
+    case 4: {  // latency_based: rolling e2e window per engine (router.cpp:130-139)
+      const int e = c.lane;
+      double lat = kInf;
+      if (e < n) {
+        EngSm& g = c.eng[e];
+        const NxEngineDesc& ed = c.ed[e];
+        const double* lt = c.P->lat_t + ed.lat_off;
+        const double* le = c.P->lat_e2e + ed.lat_off;
+        const double horizon = now - d.lat_window;
+        int head = g.lat_head, len = g.lat_len;
+        double sum = g.lat_sum;
+        while (len > 0 && lt[head] < horizon) {
+          sum -= le[head];
+          head = (head + 1) % ed.lat_cap;
+          --len;
+        }
+        g.lat_head = head;  // engine-owned fields: lane e is the only writer
+        g.lat_len = len;
+        g.lat_sum = sum;
+        lat = len == 0 ? 0.0 : sum / static_cast<double>(len);
+      }
+      __syncwarp();
+      // first strict minimum (NaN never wins)
+      double v = (e < n && !isnan(lat)) ? lat : kInf;
+      int who = e < n ? e : 64;
+      if (e < n && isnan(lat)) who = 63;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(NX_FULL, v, o);
+        const int ow = __shfl_xor_sync(NX_FULL, who, o);
+        if (ov < v || (ov == v && ow < who)) {
+          v = ov;
+          who = ow;
+        }
+      }
+      chosen = (v == kInf) ? 0 : who;
+      break;
+    }
+    case 5: {  // weighted draw (router.cpp:186-203)
+      if (c.lane == 0) {
+        double total = 0.0;
+        for (int e = 0; e < n; ++e) total += c.ed[e].static_w;
+        Rng rng;
+        for (int i = 0; i < 4; ++i) rng.s[i] = c.rs->rng[i];
+        double draw = rng.uniform() * total;
+        for (int i = 0; i < 4; ++i) c.rs->rng[i] = rng.s[i];
+        chosen = n - 1;
+        for (int e = 0; e < n; ++e) {
+          draw -= c.ed[e].static_w;
+          if (draw <= 0.0) {
+            chosen = e;
+            break;
+          }
+        }
+      }
+      chosen = __shfl_sync(NX_FULL, chosen, 0);
+      __syncwarp();
+      break;
+    }
+    default: {  // PRISM multiplicative score (router.cpp:205-284)
+      const int prompt = c.P->prompt[c.roff + rid];
+      const double dem = static_cast<double>(prompt) + c.rs->l_bar_ema;
+      const double demand = (1.0 < dem) ? dem : 1.0;
+      const int e = c.lane;
+      const bool on = e < n;
+      double score = -kInf, rho = 0.0;
+      int id = 0x7fffffff;
+      bool fresh = false;
+      if (on) {
+        const EngSm& g = c.eng[e];
+        id = c.ed[e].engine_id;
+        double f0 = 1.0, f1 = 1.0, f2 = 1.0, f3;
+        const double age = g.has_rep ? now - g.rep_at : kInf;
+        if (g.has_rep && age <= d.stale_limit) {
+          fresh = true;
+          const double knee = d.knee * d.ttft_slo;
+          if (g.rep_lhat <= knee) f0 = 1.0;
+          else {
+            const double scale = d.scale_ms > 0.0 ? d.scale_ms : 0.25 * d.ttft_slo;
+            f0 = exp(-(g.rep_lhat - knee) / scale);
+          }
+          f1 = score_load(g.rep_wload, g.rep_pmax, d.load_half);
+          const double rr = g.rep_mfree / (d.headroom * demand);
+          const double cl = (rr < 0.0) ? 0.0 : ((1.0 < rr) ? 1.0 : rr);
+          f2 = cl * cl;
+          rho = g.rep_wload / g.rep_pmax;
+        } else {
+          f0 = 0.5;
+          f2 = 0.5;
+          if (g.has_rep) {
+            rho = g.rep_wload / g.rep_pmax;
+            const double blend = exp(-(age - d.stale_limit) / d.stale_limit);
+            f1 = 1.0 + (score_load(g.rep_wload, g.rep_pmax, d.load_half) - 1.0) * blend;
+          }
+        }
+        f3 = sess_eng[sess] == e ? d.beta_aff : 1.0;
+        const double f[4] = {f0, f1, f2, f3};
+        score = 1.0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const double w = d.weights[i];
+          double term;
+          if (f[i] == 0.0 && w > 0.0) term = 0.0;
+          else if (w == 1.0) term = f[i];  // pow(x, 1) == x exactly
+          else if (w == 0.0) term = 1.0;   // pow(x, 0) == 1
+          else term = pow(f[i], w);
+          score *= term;
+        }
+      }
+      // argmax on (score desc, rho asc, id asc) — the sequential scan's "better"
+      int who = on ? e : 64;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double os = __shfl_xor_sync(NX_FULL, score, o);
+        const double orho = __shfl_xor_sync(NX_FULL, rho, o);
+        const int oid = __shfl_xor_sync(NX_FULL, id, o);
+        const int ow = __shfl_xor_sync(NX_FULL, who, o);
+        const bool better = os > score || (os == score && (orho < rho || (orho == rho && oid < id)));
+        if (better) {
+          score = os;
+          rho = orho;
+          id = oid;
+          who = ow;
+        }
+      }
+      chosen = who;
+      if (!__any_sync(NX_FULL, fresh)) chosen = least_loaded(c);  // degraded
+      __syncwarp();
+      if (c.lane == 0) {  // dispatch echo (router.cpp:275-282)
+        EngSm& g = c.eng[chosen];
+        if (g.has_rep) {
+          g.rep_qlen += 1;
+          g.rep_wload += static_cast<double>(prompt) + 32.0;
+        }
+      }
+      __syncwarp();
+      break;
+    }
+  }
+  __syncwarp();
+  if (c.lane == 0) sess_eng[sess] = chosen;  // remember_session (router.cpp:107-122)
+  __syncwarp();
+  return chosen;
+}
+
+// ---- replica driver -------------------------------------------------------------
+__device__ void init_replica(Ctx& c) {
+  const NxReplicaDesc& d = *c.d;
+  for (int e = c.lane; e < c.n_eng; e += 32) {
+    EngSm& g = c.eng[e];
+    const NxEngineDesc& ed = c.ed[e];
+    // OnlineLearner::default_priors (learner.cpp:117-128)
+    g.lp.p_max = 20.0; g.lp.kB = 0.1; g.lp.kS = 0.02; g.lp.tau0 = 5.0;
+    g.lp.w0 = 0.0; g.lp.ws = 1.0; g.lp.tauB = 0.1; g.lp.tauS = 0.001;
+    g.alpha = d.alpha; g.beta = d.beta; g.l_bar = d.l_bar; g.td_min = d.td_min;
+    g.plan_pred = 0.0; g.plan_target = 0.0; g.actual = 0.0; g.learn_y = 0.0; g.lat_sum = 0.0;
+    g.rep_lhat = 0.0; g.rep_wload = 0.0; g.rep_mfree = 0.0; g.rep_pmax = 1.0; g.rep_at = 0.0;
+    for (int i = 0; i < 4; ++i) g.rng[i] = ed.rng[i];
+    g.step_t = kNoEvent; g.learn_t = kNoEvent;
+    g.report_t = 0; g.report_seq = static_cast<uint32_t>(e);  // initial reports: seq 0..E-1
+    g.step_seq = 0; g.learn_seq = 0;
+    g.started_us = 0; g.seen = 0; g.rep_qlen = 0; g.tw_degen = 0;
+    for (int i = 0; i < 7; ++i) g.cnt[i] = 0;
+    g.wq_head = 0; g.wq_len = 0; g.rq_len = 0;
+    g.pinned = 0; g.reserved = 0; g.cache_blocks = 0; g.lru_head = -1; g.lru_tail = -1;
+    g.busy = 0; g.plan_n = 0; g.plan_b = 0; g.plan_s = 0; g.plan_wspan = 0; g.plan_overload = 0;
+    g.learn_b = 0; g.learn_s = 0;
+    g.ring_size = 0; g.ring_head = 0; g.tw_head = 0; g.tw_len = 0;
+    g.dq_head = 0; g.dq_len = 0; g.lat_head = 0; g.lat_len = 0; g.has_rep = 0;
+  }
+  if (c.lane == 0) {
+    RepSm& R = *c.rs;
+    R.ev_hash = 0xcbf29ce484222325ULL;
+    R.rr_next = 0;
+    for (int i = 0; i < 4; ++i) R.rng[i] = d.router_rng[i];
+    R.arrived = 0; R.rejected = 0; R.pending = c.n_req; R.n_rec = 0; R.events = 0; R.info = 0;
+    R.l_bar_ema = 128.0;
+    R.next_seq = static_cast<uint32_t>(c.n_eng + c.n_req);  // arrival i carries seq E + i
+    R.cursor = 0; R.status = 0; R.site = 0;
+  }
+  __syncwarp();
+}
+
+__device__ void run_replica(Ctx& c) {
+  init_replica(c);
+  const NxReplicaDesc& d = *c.d;
+  const uint64_t duration = static_cast<uint64_t>(d.duration_us);
+  while (!failed(c)) {
+    // ---- next event: warp-wide (time, seq) minimum over the slots ----
+    uint64_t t = kNoEvent;
+    uint32_t sq = 0xffffffffu;
+    int kind = -1;
+    if (c.lane < c.n_eng) {
+      const EngSm& g = c.eng[c.lane];
+      if (g.step_t != kNoEvent) { t = g.step_t; sq = g.step_seq; kind = 1; }
+      if (g.report_t < t || (g.report_t == t && g.report_t != kNoEvent && g.report_seq < sq)) {
+        t = g.report_t; sq = g.report_seq; kind = 2;
+      }
+      if (g.learn_t < t || (g.learn_t == t && g.learn_t != kNoEvent && g.learn_seq < sq)) {
+        t = g.learn_t; sq = g.learn_seq; kind = 3;
+      }
+      if (g.dq_len > 0) {
+        const int64_t o = c.ed[c.lane].dq_off + g.dq_head;
+        const uint64_t dt = static_cast<uint64_t>(c.P->dq_t[o]);
+        const uint32_t ds = c.P->dq_seq[o];
+        if (dt < t || (dt == t && ds < sq)) { t = dt; sq = ds; kind = 4; }
+      }
+    }
+    if (c.lane == 0 && c.rs->cursor < c.n_req) {
+      const uint64_t at = static_cast<uint64_t>(c.P->arr_us[c.roff + c.rs->cursor]);
+      const uint32_t as = static_cast<uint32_t>(c.n_eng + c.rs->cursor);
+      if (at < t || (at == t && as < sq)) { t = at; sq = as; kind = 0; }
+    }
+    const uint32_t hi = static_cast<uint32_t>(t >> 32), lo = static_cast<uint32_t>(t);
+    const uint32_t mhi = __reduce_min_sync(NX_FULL, hi);
+    const uint32_t mlo = __reduce_min_sync(NX_FULL, hi == mhi ? lo : 0xffffffffu);
+    const bool tie = hi == mhi && lo == mlo;
+    const uint32_t msq = __reduce_min_sync(NX_FULL, tie ? sq : 0xffffffffu);
+    const uint64_t now_u = (static_cast<uint64_t>(mhi) << 32) | mlo;
+    if (now_u == kNoEvent || now_u > duration) break;
+    const unsigned win = __ballot_sync(NX_FULL, tie && sq == msq && kind >= 0);
+    const int wl = __ffs(win) - 1;
+    kind = __shfl_sync(NX_FULL, kind, wl);
+    const int who = wl;  // engine index for engine events
+    const int64_t now = static_cast<int64_t>(now_u);
+    // ---- consume the slot ----
+    int rid = 0;
+    double dv[5];
+    int64_t dq_q = 0;
+    if (kind == 0) rid = c.rs->cursor;
+    if (kind == 4) {
+      const int64_t o = c.ed[who].dq_off + c.eng[who].dq_head;
+      for (int i = 0; i < 5; ++i) dv[i] = c.P->dq_sv[5 * o + i];
+      dq_q = c.P->dq_qlen[o];
+    }
+    __syncwarp();
+    if (c.lane == 0) {
+      EngSm& g = c.eng[kind == 0 ? 0 : who];
+      if (kind == 0) c.rs->cursor += 1;
+      else if (kind == 1) g.step_t = kNoEvent;
+      else if (kind == 2) g.report_t = kNoEvent;
+      else if (kind == 3) g.learn_t = kNoEvent;
+      else {
+        g.dq_head = (g.dq_head + 1) % c.ed[who].dq_cap;
+        g.dq_len -= 1;
+      }
+    }
+    __syncwarp();
+    // periodic reports keep no work alive (sim.cpp:295-300)
+    if (kind == 2 && c.rs->pending == 0 && c.rs->arrived - c.rs->rejected - c.rs->n_rec == 0) continue;
+    __syncwarp();
+    if (c.lane == 0) {
+      uint64_t h = c.rs->ev_hash;
+      h = fnv1a(h, now_u);
+      h = fnv1a(h, static_cast<uint64_t>(kind));
+      h = fnv1a(h, kind == 0 ? 0ull : static_cast<uint64_t>(c.ed[who].engine_id + 1));
+      h = fnv1a(h, static_cast<uint64_t>(rid));
+      c.rs->ev_hash = h;
+      c.rs->events += 1;
+    }
+    __syncwarp();
+    switch (kind) {
+      case 0: {  // arrival (sim.cpp:168-194)
+        __syncwarp();
+        if (c.lane == 0) {
+          c.rs->arrived += 1;
+          c.rs->pending -= 1;
+        }
+        __syncwarp();
+        const int e = route(c, rid, to_ms(now));
+        if (failed(c)) break;
+        int ok = 0;
+        if (c.lane == 0) {
+          ok = admit(c, e, rid) ? 1 : 0;
+          if (!ok) c.rs->rejected += 1;
+        }
+        ok = __shfl_sync(NX_FULL, ok, 0);
+        __syncwarp();
+        if (ok) try_begin_step(c, e, now);
+        break;
+      }
+      case 1:
+        step_complete(c, who, now);
+        break;
+      case 2:
+        state_report(c, who, now);
+        break;
+      case 3: {
+        const EngSm& g = c.eng[who];
+        record_sample(c, who, g.learn_b, g.learn_s, g.learn_y);
+        break;
+      }
+      case 4: {  // report delivery -> Router::on_report (router.cpp:75-81)
+        __syncwarp();
+        if (c.lane == 0) {
+          EngSm& g = c.eng[who];
+          g.has_rep = 1;
+          g.rep_lhat = dv[0];
+          g.rep_wload = dv[1];
+          g.rep_mfree = dv[2];
+          g.rep_pmax = dv[3];
+          g.rep_at = dv[4];
+          g.rep_qlen = dq_q;
+        }
+        __syncwarp();
+        break;
+      }
+    }
+  }
+}
+
+__device__ void write_outputs(Ctx& c, int r) {
+  __syncwarp();
+  NxReplicaOut& o = c.P->rep_out[r];
+  if (c.lane == 0) {
+    const RepSm& R = *c.rs;
+    o.arrived = R.arrived;
+    o.rejected = R.rejected;
+    o.completed = R.n_rec;
+    o.pending = R.pending;
+    o.events = R.events;
+    o.event_hash = R.ev_hash;
+    o.status = R.status;
+    o.err_site = R.site;
+    o.err_info = R.info;
+  }
+  for (int e = c.lane; e < c.n_eng; e += 32) {
+    const EngSm& g = c.eng[e];
+    NxEngineOut& eo = c.P->eng_out[c.d->eng_base + e];
+    params_to(g.lp, eo.params);
+    eo.samples = g.seen;
+    for (int i = 0; i < 7; ++i) eo.counters[i] = g.cnt[i];
+    eo.tradeoff_degenerate = g.tw_degen;
+    eo.alpha = g.alpha;
+    eo.beta = g.beta;
+    eo.l_bar = g.l_bar;
+  }
+  __syncwarp();
+}
+
+}  // namespace nxd
+
+// One warp per replica; warps pull replica indices (in host-chosen order,
+// longest first) from a global counter so a long replica never blocks a block.
+extern "C" __global__ void __launch_bounds__(128)
+nx_sim_kernel(const NxPools* __restrict__ pools, const int32_t* __restrict__ order, int n_rep,
+              int* next_rep, int smem_per_warp, int prefix_cap) {
+  using namespace nxd;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int warp = threadIdx.x >> 5;
+  unsigned char* base = smem + static_cast<size_t>(warp) * smem_per_warp;
+  Ctx c;
+  c.P = pools;
+  c.lane = lane_id();
+  c.rs = reinterpret_cast<RepSm*>(base);
+  const size_t rep_bytes = (sizeof(RepSm) + 15) & ~size_t(15);
+  c.chunk = reinterpret_cast<double*>(base + rep_bytes);
+  c.prefix = reinterpret_cast<int32_t*>(base + rep_bytes);
+  const size_t stage = ((static_cast<size_t>(prefix_cap) * 4 > 32 * 5 * 8 ? static_cast<size_t>(prefix_cap) * 4
+                                                                        : 32 * 5 * 8) + 15) & ~size_t(15);
+  c.eng = reinterpret_cast<EngSm*>(base + rep_bytes + stage);
+  c.prefix_cap = prefix_cap;
+  while (true) {
+    int slot = 0;
+    if (c.lane == 0) slot = atomicAdd(next_rep, 1);
+    slot = __shfl_sync(NX_FULL, slot, 0);
+    if (slot >= n_rep) break;
+    const int r = order[slot];
+    c.d = pools->rep + r;
+    c.ed = pools->eng + c.d->eng_base;
+    c.n_eng = c.d->n_eng;
+    c.n_req = c.d->n_req;
+    c.n_sess = c.d->n_sess;
+    c.roff = c.d->req_off;
+    c.soff = c.d->sess_off;
+    c.scratch = pools->scratch + c.d->scratch_off;
+    run_replica(c);
+    write_outputs(c, r);
+  }
+}
+
+// Size of the per-warp shared-memory slice (host uses the same formula).
+extern "C" size_t nx_sim_smem_per_warp(int max_engines, int prefix_cap) {
+  using namespace nxd;
+  const size_t rep_bytes = (sizeof(RepSm) + 15) & ~size_t(15);
+  const size_t stage = ((static_cast<size_t>(prefix_cap) * 4 > 32 * 5 * 8 ? static_cast<size_t>(prefix_cap) * 4
+                                                                        : 32 * 5 * 8) + 15) & ~size_t(15);
+  return rep_bytes + stage + sizeof(EngSm) * static_cast<size_t>(max_engines);
+}
+
+extern "C" cudaError_t nx_launch_sim(const NxPools* d_pools, const int32_t* d_order, int n_rep,
+                                     int* d_next, int smem_per_warp, int prefix_cap, int grid,
+                                     int warps_per_block, cudaStream_t st) {
+  const size_t smem = static_cast<size_t>(smem_per_warp) * warps_per_block;
+  cudaError_t err = cudaFuncSetAttribute(nx_sim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+  if (err != cudaSuccess) return err;
+  nx_sim_kernel<<<grid, 32 * warps_per_block, smem, st>>>(d_pools, d_order, n_rep, d_next,
+                                                          smem_per_warp, prefix_cap);
+  return cudaGetLastError();
+}
+
+extern "C" cudaError_t nx_sim_occupancy(int warps_per_block, size_t smem, int* blocks_per_sm) {
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, nx_sim_kernel,
+                                                       32 * warps_per_block, smem);
+}

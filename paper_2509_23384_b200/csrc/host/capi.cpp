@@ -1,0 +1,714 @@
+// C-ABI implementation (include/nx_sched.h): packs RunConfig batches into the
+// SoA image of nx_layout.h, moves it to HBM, launches the device kernels and
+// returns reference-shaped results. No simulation logic lives here — every
+// scheduling decision is made on the device (csrc/device/*.cu).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <numeric>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../nx_layout.h"
+#include "frontend.hpp"
+#include "nx_sched.h"
+#include "report.hpp"
+
+extern "C" cudaError_t nx_launch_sim(const NxPools* d_pools, const int32_t* d_order, int n_rep,
+                                     int* d_next, int smem_per_warp, int prefix_cap, int grid,
+                                     int warps_per_block, cudaStream_t st);
+extern "C" cudaError_t nx_sim_occupancy(int warps_per_block, size_t smem, int* blocks_per_sm);
+extern "C" size_t nx_sim_smem_per_warp(int max_engines, int prefix_cap);
+extern "C" cudaError_t nx_launch_perf_eval(const double* params, int n_params, const int32_t* idx,
+                                           const int32_t* b, const int32_t* s, double* outT,
+                                           double* outThr, int64_t n, int fp32, unsigned* bad,
+                                           int sms, cudaStream_t st);
+
+namespace {
+
+thread_local std::string g_err;
+
+struct NxError : std::runtime_error {
+  int code;
+  NxError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw NxError(NX_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return NX_OK;
+  } catch (const NxError& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return NX_EINVAL;
+  } catch (const std::logic_error& e) {
+    g_err = e.what();
+    return NX_ELOGIC;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return NX_ERUNTIME;
+  }
+}
+
+int sm_count(int device) {
+  int n = 0;
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device);
+  return n > 0 ? n : 148;
+}
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+// Device arena: one allocation, sub-buffers at 256-B aligned offsets.
+struct Arena {
+  size_t size = 0;
+  template <class T>
+  size_t take(size_t count) {
+    const size_t off = align_up(size, 256);
+    size = off + sizeof(T) * std::max<size_t>(count, 1);
+    return off;
+  }
+};
+
+constexpr int kWarpsPerBlock = 4;
+
+}  // namespace
+
+struct nx_sim {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  std::vector<nx::RunCfg> cfgs;
+  std::vector<nx::Workload> wl;
+  int n_rep = 0, max_eng = 1, prefix_cap = 1;
+  int64_t n_req = 0, n_sess = 0, n_eng = 0;
+  // host pinned input image
+  std::vector<NxReplicaDesc> rep;
+  std::vector<NxEngineDesc> eng;
+  std::vector<int32_t> order;
+  int64_t* h_arr_us = nullptr;
+  double* h_arr_ms = nullptr;
+  int32_t* h_prompt = nullptr;
+  int32_t* h_target = nullptr;
+  int32_t* h_session = nullptr;
+  // host pinned outputs
+  NxReplicaOut* h_rep_out = nullptr;
+  NxEngineOut* h_eng_out = nullptr;
+  int32_t* h_records = nullptr;
+  int64_t* h_first_us = nullptr;
+  int64_t* h_done_us = nullptr;
+  int32_t* h_req_engine = nullptr;
+  // device
+  unsigned char* d_arena = nullptr;
+  size_t arena_bytes = 0;
+  NxPools pools{};
+  NxPools* d_pools = nullptr;
+  int32_t* d_order = nullptr;
+  int* d_next = nullptr;
+  size_t off_rep = 0, off_eng = 0, off_rep_out = 0, off_eng_out = 0;
+  size_t off_state_begin = 0, off_state_end = 0;  // zero-initialised state span
+  size_t off_ff_begin = 0, off_ff_end = 0;        // 0xff-initialised span
+  int64_t h2d_bytes = 0, d2h_bytes = 0;
+  float last_ms = 0.f;
+  bool launched = false;
+
+  ~nx_sim() {
+    if (d_arena) cudaFree(d_arena);
+    if (d_pools) cudaFree(d_pools);
+    for (void* p : {(void*)h_arr_us, (void*)h_arr_ms, (void*)h_prompt, (void*)h_target,
+                    (void*)h_session, (void*)h_rep_out, (void*)h_eng_out, (void*)h_records,
+                    (void*)h_first_us, (void*)h_done_us, (void*)h_req_engine})
+      if (p) cudaFreeHost(p);
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
+namespace {
+
+template <class T>
+T* pinned(size_t count) {
+  void* p = nullptr;
+  cuda_check(cudaMallocHost(&p, sizeof(T) * std::max<size_t>(count, 1)), "cudaMallocHost");
+  return static_cast<T*>(p);
+}
+
+void fill_descriptors(nx_sim& h) {
+  h.rep.resize(h.n_rep);
+  h.eng.clear();
+  int64_t req_off = 0, sess_off = 0, scratch_off = 0;
+  // pool element offsets (per engine regions)
+  int64_t wq_off = 0, rq_off = 0, plan_off = 0, cache_off = 0, ring_off = 0, tw_off = 0, dq_off = 0,
+          lat_off = 0;
+  for (int r = 0; r < h.n_rep; ++r) {
+    const nx::RunCfg& c = h.cfgs[r];
+    const nx::Workload& w = h.wl[r];
+    const int n = static_cast<int>(w.prompt.size());
+    const int ns = static_cast<int>(w.session_names.size());
+    NxReplicaDesc& d = h.rep[r];
+    std::memset(&d, 0, sizeof d);
+    d.ttft_slo = c.ttft_slo;
+    d.tpot_slo = c.tpot_slo;
+    d.eps_ratio = c.eps_ratio;
+    d.q_ref = c.q_ref;
+    d.alpha = c.alpha;
+    d.beta = c.beta;
+    d.l_bar = c.l_bar;
+    d.td_min = c.td_min;
+    for (int i = 0; i < 4; ++i) d.weights[i] = c.weights[i];
+    d.beta_aff = c.beta_aff;
+    d.knee = c.knee;
+    d.scale_ms = c.scale_ms;
+    d.load_half = c.load_half;
+    d.headroom = c.headroom;
+    d.stale_limit = c.staleness_limit;
+    d.lat_window = c.latency_window;
+    nx::Xoshiro rr(nx::substream_seed(c.seed, "router"));
+    for (int i = 0; i < 4; ++i) d.router_rng[i] = rr.s[i];
+    d.duration_us = nx::to_us(c.duration_ms);
+    d.req_off = req_off;
+    d.sess_off = sess_off;
+    d.scratch_off = scratch_off;
+    d.n_eng = static_cast<int32_t>(c.engines.size());
+    d.eng_base = static_cast<int32_t>(h.eng.size());
+    d.n_req = n;
+    d.n_sess = ns;
+    d.n_iters = c.n_search_iters;
+    d.route_policy = c.route_policy;
+    d.long_w = static_cast<int32_t>(c.long_window);
+    d.short_w = static_cast<int32_t>(c.short_window);
+    d.s_period = static_cast<int32_t>(c.structural_period);
+    d.l_period = static_cast<int32_t>(c.linear_period);
+    d.min_s = static_cast<int32_t>(std::min<int64_t>(c.min_structural, INT32_MAX));
+    req_off += n;
+    sess_off += ns;
+    scratch_off += static_cast<int64_t>(c.long_window) + 1024 + 2 * c.short_window + 64;
+    for (const auto& ec : c.engines) {
+      NxEngineDesc e;
+      std::memset(&e, 0, sizeof e);
+      const nx::Params& tp = ec.true_params;
+      const double tpv[8] = {tp.tau0, tp.w0, tp.ws, tp.tauB, tp.tauS, tp.p_max, tp.kB, tp.kS};
+      for (int i = 0; i < 8; ++i) e.tp[i] = tpv[i];
+      e.noise_sigma = ec.noise_sigma;
+      auto it = c.static_weights.find(ec.engine_id);
+      e.static_w = it != c.static_weights.end() ? it->second : 1.0;
+      e.period_us = nx::to_us(ec.report_period_ms);
+      e.stale_us = nx::to_us(ec.staleness_ms);
+      nx::Xoshiro er(nx::substream_seed(c.seed, "engine-noise", static_cast<uint64_t>(ec.engine_id)));
+      for (int i = 0; i < 4; ++i) e.rng[i] = er.s[i];
+      e.engine_id = ec.engine_id;
+      e.policy = ec.policy;
+      e.kv_blocks = static_cast<int32_t>(ec.kv_blocks);
+      e.block_size = static_cast<int32_t>(ec.block_size);
+      e.m_max = static_cast<int32_t>(ec.m_max);
+      e.q_max = static_cast<int32_t>(ec.q_max);
+      e.static_budget = static_cast<int32_t>(ec.static_budget);
+      e.wait_cap = static_cast<int32_t>(ec.wait_cap);
+      // deliveries in flight per engine: ceil(staleness / period) + 1 (+ slack)
+      const int64_t per = std::max<int64_t>(1, e.period_us);
+      e.dq_cap = static_cast<int32_t>(std::min<int64_t>(e.stale_us / per + 3, 1 << 20));
+      e.lat_cap = c.route_policy == nx::kLatencyBased ? std::max(n, 1) : 0;
+      e.wq_off = wq_off;
+      e.rq_off = rq_off;
+      e.plan_off = plan_off;
+      e.cache_off = cache_off;
+      e.ring_off = ring_off;
+      e.tw_off = tw_off;
+      e.dq_off = dq_off;
+      e.lat_off = lat_off;
+      wq_off += n;
+      rq_off += n;
+      plan_off += std::max(n, 1);
+      cache_off += ns;
+      ring_off += c.long_window;
+      tw_off += NX_TW_CAP;
+      dq_off += e.dq_cap;
+      lat_off += e.lat_cap;
+      h.eng.push_back(e);
+    }
+    h.max_eng = std::max(h.max_eng, d.n_eng);
+    for (const auto& ec : c.engines)
+      h.prefix_cap = std::max<int>(h.prefix_cap, static_cast<int>(ec.q_max) + 1);
+  }
+  h.n_req = req_off;
+  h.n_sess = sess_off;
+  h.n_eng = static_cast<int64_t>(h.eng.size());
+
+  // device arena layout
+  Arena A;
+  const size_t o_arr_us = A.take<int64_t>(h.n_req);
+  const size_t o_arr_ms = A.take<double>(h.n_req);
+  const size_t o_prompt = A.take<int32_t>(h.n_req);
+  const size_t o_target = A.take<int32_t>(h.n_req);
+  const size_t o_session = A.take<int32_t>(h.n_req);
+  h.off_rep = A.take<NxReplicaDesc>(h.n_rep);
+  h.off_eng = A.take<NxEngineDesc>(h.n_eng);
+  const size_t o_order = A.take<int32_t>(h.n_rep);
+  // zero-initialised state
+  h.off_state_begin = align_up(A.size, 256);
+  const size_t o_prefilled = A.take<int32_t>(h.n_req);
+  const size_t o_decoded = A.take<int32_t>(h.n_req);
+  const size_t o_kv = A.take<uint8_t>(h.n_req);
+  const size_t o_next = A.take<int>(1);
+  h.off_state_end = A.size;
+  // 0xff-initialised (-1) state
+  h.off_ff_begin = align_up(A.size, 256);
+  const size_t o_sess_eng = A.take<int32_t>(h.n_sess);
+  const size_t o_ctok = A.take<int32_t>(cache_off);
+  h.off_ff_end = A.size;
+  // uninitialised state
+  const size_t o_first = A.take<int64_t>(h.n_req);
+  const size_t o_done = A.take<int64_t>(h.n_req);
+  const size_t o_reqeng = A.take<int32_t>(h.n_req);
+  const size_t o_wq = A.take<int32_t>(wq_off);
+  const size_t o_rq = A.take<int32_t>(rq_off);
+  const size_t o_preq = A.take<int32_t>(plan_off);
+  const size_t o_ptok = A.take<int32_t>(plan_off);
+  const size_t o_cprev = A.take<int32_t>(cache_off);
+  const size_t o_cnext = A.take<int32_t>(cache_off);
+  const size_t o_rb = A.take<int32_t>(ring_off);
+  const size_t o_rs = A.take<int32_t>(ring_off);
+  const size_t o_ry = A.take<double>(ring_off);
+  const size_t o_twt = A.take<double>(tw_off);
+  const size_t o_twp = A.take<double>(tw_off);
+  const size_t o_dqt = A.take<int64_t>(dq_off);
+  const size_t o_dqs = A.take<uint32_t>(dq_off);
+  const size_t o_dqv = A.take<double>(5 * dq_off);
+  const size_t o_dqq = A.take<int64_t>(dq_off);
+  const size_t o_latt = A.take<double>(lat_off);
+  const size_t o_late = A.take<double>(lat_off);
+  const size_t o_rec = A.take<int32_t>(h.n_req);
+  const size_t o_scr = A.take<double>(scratch_off);
+  h.off_rep_out = A.take<NxReplicaOut>(h.n_rep);
+  h.off_eng_out = A.take<NxEngineOut>(h.n_eng);
+  h.arena_bytes = A.size;
+
+  cuda_check(cudaMalloc(&h.d_arena, h.arena_bytes), "cudaMalloc(arena)");
+  unsigned char* B = h.d_arena;
+  NxPools& P = h.pools;
+  P.arr_us = reinterpret_cast<const int64_t*>(B + o_arr_us);
+  P.arr_ms = reinterpret_cast<const double*>(B + o_arr_ms);
+  P.prompt = reinterpret_cast<const int32_t*>(B + o_prompt);
+  P.target = reinterpret_cast<const int32_t*>(B + o_target);
+  P.session = reinterpret_cast<const int32_t*>(B + o_session);
+  P.prefilled = reinterpret_cast<int32_t*>(B + o_prefilled);
+  P.decoded = reinterpret_cast<int32_t*>(B + o_decoded);
+  P.first_us = reinterpret_cast<int64_t*>(B + o_first);
+  P.done_us = reinterpret_cast<int64_t*>(B + o_done);
+  P.req_engine = reinterpret_cast<int32_t*>(B + o_reqeng);
+  P.kv_admitted = reinterpret_cast<uint8_t*>(B + o_kv);
+  P.wq = reinterpret_cast<int32_t*>(B + o_wq);
+  P.rq = reinterpret_cast<int32_t*>(B + o_rq);
+  P.plan_req = reinterpret_cast<int32_t*>(B + o_preq);
+  P.plan_tok = reinterpret_cast<int32_t*>(B + o_ptok);
+  P.c_tokens = reinterpret_cast<int32_t*>(B + o_ctok);
+  P.c_prev = reinterpret_cast<int32_t*>(B + o_cprev);
+  P.c_next = reinterpret_cast<int32_t*>(B + o_cnext);
+  P.ring_b = reinterpret_cast<int32_t*>(B + o_rb);
+  P.ring_s = reinterpret_cast<int32_t*>(B + o_rs);
+  P.ring_y = reinterpret_cast<double*>(B + o_ry);
+  P.tw_ttft = reinterpret_cast<double*>(B + o_twt);
+  P.tw_tpot = reinterpret_cast<double*>(B + o_twp);
+  P.dq_t = reinterpret_cast<int64_t*>(B + o_dqt);
+  P.dq_seq = reinterpret_cast<uint32_t*>(B + o_dqs);
+  P.dq_sv = reinterpret_cast<double*>(B + o_dqv);
+  P.dq_qlen = reinterpret_cast<int64_t*>(B + o_dqq);
+  P.lat_t = reinterpret_cast<double*>(B + o_latt);
+  P.lat_e2e = reinterpret_cast<double*>(B + o_late);
+  P.sess_engine = reinterpret_cast<int32_t*>(B + o_sess_eng);
+  P.records = reinterpret_cast<int32_t*>(B + o_rec);
+  P.scratch = reinterpret_cast<double*>(B + o_scr);
+  P.rep = reinterpret_cast<const NxReplicaDesc*>(B + h.off_rep);
+  P.eng = reinterpret_cast<const NxEngineDesc*>(B + h.off_eng);
+  P.rep_out = reinterpret_cast<NxReplicaOut*>(B + h.off_rep_out);
+  P.eng_out = reinterpret_cast<NxEngineOut*>(B + h.off_eng_out);
+  h.d_order = reinterpret_cast<int32_t*>(B + o_order);
+  h.d_next = reinterpret_cast<int*>(B + o_next);
+  cuda_check(cudaMalloc(&h.d_pools, sizeof(NxPools)), "cudaMalloc(pools)");
+  cuda_check(cudaMemcpy(h.d_pools, &h.pools, sizeof(NxPools), cudaMemcpyHostToDevice),
+             "cudaMemcpy(pools)");
+
+  // pinned host image of the inputs
+  h.h_arr_us = pinned<int64_t>(h.n_req);
+  h.h_arr_ms = pinned<double>(h.n_req);
+  h.h_prompt = pinned<int32_t>(h.n_req);
+  h.h_target = pinned<int32_t>(h.n_req);
+  h.h_session = pinned<int32_t>(h.n_req);
+  for (int r = 0; r < h.n_rep; ++r) {
+    const nx::Workload& w = h.wl[r];
+    const int64_t o = h.rep[r].req_off;
+    const size_t n = w.prompt.size();
+    std::memcpy(h.h_arr_us + o, w.arrival_us.data(), n * sizeof(int64_t));
+    std::memcpy(h.h_arr_ms + o, w.arrival_ms.data(), n * sizeof(double));
+    std::memcpy(h.h_prompt + o, w.prompt.data(), n * sizeof(int32_t));
+    std::memcpy(h.h_target + o, w.output.data(), n * sizeof(int32_t));
+    std::memcpy(h.h_session + o, w.session.data(), n * sizeof(int32_t));
+  }
+  // longest-expected replicas first: more requests and lower rates run longer
+  h.order.resize(h.n_rep);
+  std::iota(h.order.begin(), h.order.end(), 0);
+  std::vector<double> cost(h.n_rep);
+  for (int r = 0; r < h.n_rep; ++r) {
+    const auto& w = h.wl[r];
+    const double span = w.arrival_ms.empty() ? 0.0 : w.arrival_ms.back();
+    cost[r] = static_cast<double>(w.prompt.size()) + span * 0.05;
+  }
+  std::stable_sort(h.order.begin(), h.order.end(), [&](int a, int b) { return cost[a] > cost[b]; });
+  h.h_rep_out = pinned<NxReplicaOut>(h.n_rep);
+  h.h_eng_out = pinned<NxEngineOut>(h.n_eng);
+  h.h_records = pinned<int32_t>(h.n_req);
+  h.h_first_us = pinned<int64_t>(h.n_req);
+  h.h_done_us = pinned<int64_t>(h.n_req);
+  h.h_req_engine = pinned<int32_t>(h.n_req);
+}
+
+const char* site_name(int site) {
+  switch (site) {
+    case NX_SITE_BISECT: return "binary_search_budget: invalid inputs";
+    case NX_SITE_ALLOCATE: return "allocate_tokens: budget below queue needs";
+    case NX_SITE_PREFILL_CAP: return "prefill_priority: prompt exceeds m_max";
+    case NX_SITE_SAMPLE: return "invalid LatencySample";
+    case NX_SITE_CAPACITY: return "score_capacity: demand must be >= 1 token";
+    case NX_SITE_OVERFLOW: return "device capacity exceeded";
+    case NX_SITE_PARAMS: return "PerfParams violate invariants";
+  }
+  return "error";
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* nx_last_error(void) { return g_err.c_str(); }
+
+int nx_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+  return n;
+}
+
+int nx_sim_create_json(const char* const* configs, int32_t n_replicas, int32_t device,
+                       int32_t host_threads, nx_sim_t* out) {
+  *out = nullptr;
+  return guard([&] {
+    if (n_replicas < 1) throw std::invalid_argument("nx_sim_create_json: no replicas");
+    auto h = std::make_unique<nx_sim>();
+    h->device = device;
+    h->n_rep = n_replicas;
+    h->cfgs.resize(n_replicas);
+    h->wl.resize(n_replicas);
+    // parse + synthesise on host threads (reference semantics, host libm)
+    std::atomic<int> next{0};
+    std::vector<std::string> errs(n_replicas);
+    std::vector<int> codes(n_replicas, 0);
+    auto work = [&] {
+      for (int i = next++; i < n_replicas; i = next++) {
+        codes[i] = guard([&] {
+          h->cfgs[i] = nx::parse_run_config(configs[i]);
+          if (h->cfgs[i].engines.size() > NX_MAX_ENGINES)
+            throw std::invalid_argument("device path supports at most 32 engines per replica");
+          h->wl[i] = nx::build_workload(h->cfgs[i]);
+          if (h->wl[i].prompt.size() > (1u << 30))
+            throw std::invalid_argument("too many requests for one replica");
+        });
+        if (codes[i]) errs[i] = g_err;
+      }
+    };
+    const int nt = std::max(1, std::min<int>(host_threads > 0 ? host_threads : 1, n_replicas));
+    std::vector<std::thread> pool;
+    for (int t = 1; t < nt; ++t) pool.emplace_back(work);
+    work();
+    for (auto& t : pool) t.join();
+    for (int i = 0; i < n_replicas; ++i)
+      if (codes[i]) throw NxError(codes[i], "replica " + std::to_string(i) + ": " + errs[i]);
+    cuda_check(cudaSetDevice(device), "cudaSetDevice");
+    cuda_check(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    cuda_check(cudaEventCreate(&h->ev0), "cudaEventCreate");
+    cuda_check(cudaEventCreate(&h->ev1), "cudaEventCreate");
+    fill_descriptors(*h);
+    *out = h.release();
+  });
+}
+
+int nx_sim_upload(nx_sim_t h) {
+  return guard([&] {
+    cuda_check(cudaSetDevice(h->device), "cudaSetDevice");
+    auto cp = [&](void* dst, const void* src, size_t bytes) {
+      cuda_check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, h->stream), "H2D");
+      h->h2d_bytes += static_cast<int64_t>(bytes);
+    };
+    h->h2d_bytes = 0;
+    NxPools& P = h->pools;
+    cp(const_cast<int64_t*>(P.arr_us), h->h_arr_us, h->n_req * sizeof(int64_t));
+    cp(const_cast<double*>(P.arr_ms), h->h_arr_ms, h->n_req * sizeof(double));
+    cp(const_cast<int32_t*>(P.prompt), h->h_prompt, h->n_req * sizeof(int32_t));
+    cp(const_cast<int32_t*>(P.target), h->h_target, h->n_req * sizeof(int32_t));
+    cp(const_cast<int32_t*>(P.session), h->h_session, h->n_req * sizeof(int32_t));
+    cp(h->d_arena + h->off_rep, h->rep.data(), h->rep.size() * sizeof(NxReplicaDesc));
+    cp(h->d_arena + h->off_eng, h->eng.data(), h->eng.size() * sizeof(NxEngineDesc));
+    cp(h->d_order, h->order.data(), h->order.size() * sizeof(int32_t));
+  });
+}
+
+int nx_sim_launch(nx_sim_t h) {
+  return guard([&] {
+    cuda_check(cudaSetDevice(h->device), "cudaSetDevice");
+    cudaStream_t st = h->stream;
+    cuda_check(cudaMemsetAsync(h->d_arena + h->off_state_begin, 0,
+                               h->off_state_end - h->off_state_begin, st), "memset state");
+    cuda_check(cudaMemsetAsync(h->d_arena + h->off_ff_begin, 0xff,
+                               h->off_ff_end - h->off_ff_begin, st), "memset state");
+    const int spw = static_cast<int>(nx_sim_smem_per_warp(h->max_eng, h->prefix_cap));
+    const size_t smem = static_cast<size_t>(spw) * kWarpsPerBlock;
+    int per_sm = 0;
+    cuda_check(nx_sim_occupancy(kWarpsPerBlock, smem, &per_sm), "occupancy");
+    if (per_sm < 1) throw NxError(NX_ECUDA, "simulation kernel does not fit on an SM");
+    const int need = (h->n_rep + kWarpsPerBlock - 1) / kWarpsPerBlock;
+    const int grid = std::max(1, std::min(need, per_sm * sm_count(h->device)));
+    cuda_check(cudaEventRecord(h->ev0, st), "event");
+    cuda_check(nx_launch_sim(h->d_pools, h->d_order, h->n_rep, h->d_next, spw, h->prefix_cap, grid,
+                             kWarpsPerBlock, st), "nx_sim_kernel launch");
+    cuda_check(cudaEventRecord(h->ev1, st), "event");
+    h->launched = true;
+  });
+}
+
+int nx_sim_download(nx_sim_t h) {
+  return guard([&] {
+    cuda_check(cudaSetDevice(h->device), "cudaSetDevice");
+    auto cp = [&](void* dst, const void* src, size_t bytes) {
+      cuda_check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, h->stream), "D2H");
+      h->d2h_bytes += static_cast<int64_t>(bytes);
+    };
+    h->d2h_bytes = 0;
+    const NxPools& P = h->pools;
+    cp(h->h_rep_out, P.rep_out, h->n_rep * sizeof(NxReplicaOut));
+    cp(h->h_eng_out, P.eng_out, h->n_eng * sizeof(NxEngineOut));
+    cp(h->h_records, P.records, h->n_req * sizeof(int32_t));
+    cp(h->h_first_us, P.first_us, h->n_req * sizeof(int64_t));
+    cp(h->h_done_us, P.done_us, h->n_req * sizeof(int64_t));
+    cp(h->h_req_engine, P.req_engine, h->n_req * sizeof(int32_t));
+  });
+}
+
+int nx_sim_synchronize(nx_sim_t h) {
+  return guard([&] {
+    cuda_check(cudaStreamSynchronize(h->stream), "nx_sim stream");
+    if (h->launched) {
+      cuda_check(cudaEventElapsedTime(&h->last_ms, h->ev0, h->ev1), "event time");
+      h->launched = false;
+    }
+  });
+}
+
+int nx_sim_run(nx_sim_t h) {
+  int rc = nx_sim_upload(h);
+  if (!rc) rc = nx_sim_launch(h);
+  if (!rc) rc = nx_sim_download(h);
+  if (!rc) rc = nx_sim_synchronize(h);
+  return rc;
+}
+
+int nx_sim_last_kernel_ms(nx_sim_t h, float* ms) {
+  *ms = h->last_ms;
+  return NX_OK;
+}
+
+int nx_sim_io_bytes(nx_sim_t h, int64_t* h2d, int64_t* d2h) {
+  *h2d = h->h2d_bytes;
+  *d2h = h->d2h_bytes;
+  return NX_OK;
+}
+
+int nx_sim_replica_count(nx_sim_t h) { return h->n_rep; }
+
+int nx_sim_summaries(nx_sim_t h, nx_replica_summary* out) {
+  return guard([&] {
+    for (int r = 0; r < h->n_rep; ++r) {
+      const NxReplicaOut& o = h->h_rep_out[r];
+      const NxReplicaDesc& d = h->rep[r];
+      nx_replica_summary& s = out[r];
+      s.arrived = o.arrived;
+      s.completed = o.completed;
+      s.rejected = o.rejected;
+      s.unfinished = o.arrived - o.rejected - o.completed + o.pending;
+      s.events = o.events;
+      int64_t batches = 0;
+      for (int e = 0; e < d.n_eng; ++e) batches += h->h_eng_out[d.eng_base + e].samples;
+      s.decisions = o.arrived + batches;
+      s.arrival_hash = h->wl[r].arrival_hash;
+      s.event_hash = o.event_hash;
+      s.status = o.status;
+      s.err_site = o.err_site;
+    }
+  });
+}
+
+int nx_sim_records(nx_sim_t h, int32_t replica, nx_request_record* out, int64_t cap, int64_t* n) {
+  return guard([&] {
+    if (replica < 0 || replica >= h->n_rep) throw std::invalid_argument("replica out of range");
+    const NxReplicaDesc& d = h->rep[replica];
+    const NxReplicaOut& o = h->h_rep_out[replica];
+    const nx::Workload& w = h->wl[replica];
+    *n = o.completed;
+    const int64_t m = std::min<int64_t>(cap, o.completed);
+    for (int64_t k = 0; k < m; ++k) {
+      const int r = h->h_records[d.req_off + k];
+      nx_request_record& rec = out[k];
+      rec.request_id = r;
+      rec.arrival_ms = w.arrival_ms[r];
+      rec.first_token_ms = nx::to_ms(h->h_first_us[d.req_off + r]);
+      rec.completed_ms = nx::to_ms(h->h_done_us[d.req_off + r]);
+      rec.prompt_tokens = w.prompt[r];
+      rec.output_tokens = w.output[r];
+      rec.engine_id = h->eng[d.eng_base + h->h_req_engine[d.req_off + r]].engine_id;
+      rec.pad_ = 0;
+    }
+  });
+}
+
+int nx_sim_summary_json(nx_sim_t h, int32_t replica, char* buf, int64_t cap, int64_t* len) {
+  return guard([&] {
+    if (replica < 0 || replica >= h->n_rep) throw std::invalid_argument("replica out of range");
+    const NxReplicaOut& o = h->h_rep_out[replica];
+    if (o.status != 0) {
+      const std::string msg = site_name(o.err_site);
+      if (o.status == 1) throw std::invalid_argument(msg);
+      if (o.status == 3) throw std::logic_error(msg);
+      throw std::runtime_error(msg);
+    }
+    const NxReplicaDesc& d = h->rep[replica];
+    std::vector<nx_request_record> recs(static_cast<size_t>(o.completed));
+    int64_t n = 0;
+    if (nx_sim_records(h, replica, recs.data(), o.completed, &n) != NX_OK)
+      throw std::runtime_error(g_err);
+    std::vector<nx::RecordRow> rows(recs.size());
+    for (size_t i = 0; i < recs.size(); ++i) {
+      rows[i].request_id = recs[i].request_id;
+      rows[i].arrival_ms = recs[i].arrival_ms;
+      rows[i].first_token_ms = recs[i].first_token_ms;
+      rows[i].completed_ms = recs[i].completed_ms;
+      rows[i].prompt_tokens = recs[i].prompt_tokens;
+      rows[i].output_tokens = recs[i].output_tokens;
+      rows[i].engine_id = recs[i].engine_id;
+    }
+    const nx::RunCfg& c = h->cfgs[replica];
+    std::vector<nx::LearnerRow> learners;
+    for (int e = 0; e < d.n_eng; ++e) {
+      const NxEngineOut& eo = h->h_eng_out[d.eng_base + e];
+      learners.push_back({h->eng[d.eng_base + e].engine_id, eo.samples, eo.params[5]});
+    }
+    const nx::Metrics m = nx::summarize_records(rows, c.ttft_slo, c.tpot_slo);
+    const std::string s = nx::build_summary_json(
+        c, o.arrived, o.completed, o.rejected, o.arrived - o.rejected - o.completed + o.pending,
+        h->wl[replica].arrival_hash, o.event_hash, m, learners);
+    *len = static_cast<int64_t>(s.size());
+    if (cap > 0) {
+      const size_t k = std::min<size_t>(s.size(), static_cast<size_t>(cap - 1));
+      std::memcpy(buf, s.data(), k);
+      buf[k] = 0;
+    }
+  });
+}
+
+int nx_sim_learner(nx_sim_t h, int32_t replica, int32_t engine, double* params8, int64_t* samples,
+                   int64_t* counters7) {
+  return guard([&] {
+    if (replica < 0 || replica >= h->n_rep) throw std::invalid_argument("replica out of range");
+    const NxReplicaDesc& d = h->rep[replica];
+    if (engine < 0 || engine >= d.n_eng) throw std::invalid_argument("engine out of range");
+    const NxEngineOut& eo = h->h_eng_out[d.eng_base + engine];
+    for (int i = 0; i < 8; ++i) params8[i] = eo.params[i];
+    *samples = eo.samples;
+    for (int i = 0; i < 7; ++i) counters7[i] = eo.counters[i];
+  });
+}
+
+int nx_sim_summaries_dev(nx_sim_t h, void** dev_ptr, int64_t* bytes) {
+  *dev_ptr = h->pools.rep_out;
+  *bytes = static_cast<int64_t>(h->n_rep) * static_cast<int64_t>(sizeof(NxReplicaOut));
+  return NX_OK;
+}
+
+void nx_sim_destroy(nx_sim_t h) { delete h; }
+
+// ---- K1 --------------------------------------------------------------------------
+int nx_perf_eval_dev(const double* params, int32_t n_params, const int32_t* idx, const int32_t* b,
+                     const int32_t* s, double* out_T, double* out_thr, int64_t n, int32_t mode,
+                     void* stream) {
+  return guard([&] {
+    if (n < 0 || n_params < 1) throw std::invalid_argument("nx_perf_eval: empty parameter table");
+    for (const void* p : {(const void*)idx, (const void*)b, (const void*)s, (const void*)out_T})
+      if (reinterpret_cast<uintptr_t>(p) % 16) throw std::invalid_argument("nx_perf_eval: buffers must be 16-byte aligned");
+    if (out_thr && reinterpret_cast<uintptr_t>(out_thr) % 16)
+      throw std::invalid_argument("nx_perf_eval: buffers must be 16-byte aligned");
+    if (n == 0) return;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    static thread_local unsigned* flag = nullptr;
+    if (!flag) cuda_check(cudaMalloc(&flag, sizeof(unsigned)), "cudaMalloc(flag)");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    cuda_check(cudaMemsetAsync(flag, 0, sizeof(unsigned), st), "memset");
+    cuda_check(nx_launch_perf_eval(params, n_params, idx, b, s, out_T, out_thr, n,
+                                   mode == NX_FAST_FP32, flag, sm_count(dev), st),
+               "perf_eval launch");
+    unsigned bad = 0;
+    cuda_check(cudaMemcpyAsync(&bad, flag, sizeof bad, cudaMemcpyDeviceToHost, st), "D2H flag");
+    cuda_check(cudaStreamSynchronize(st), "perf_eval sync");
+    if (bad) throw std::invalid_argument("BatchShape requires b >= 1 and s >= b, valid params");
+  });
+}
+
+int nx_perf_eval_host(const double* params, int32_t n_params, const int32_t* idx, const int32_t* b,
+                      const int32_t* s, double* out_T, double* out_thr, int64_t n, int32_t mode) {
+  return guard([&] {
+    if (n < 0 || n_params < 1) throw std::invalid_argument("nx_perf_eval: empty parameter table");
+    unsigned char* d = nullptr;
+    Arena A;
+    const size_t op = A.take<double>(8 * static_cast<size_t>(n_params));
+    const size_t oi = A.take<int32_t>(n), ob = A.take<int32_t>(n), os = A.take<int32_t>(n);
+    const size_t oT = A.take<double>(n), oh = A.take<double>(n);
+    cuda_check(cudaMalloc(&d, A.size), "cudaMalloc");
+    std::unique_ptr<unsigned char, void (*)(unsigned char*)> hold(d, [](unsigned char* p) { cudaFree(p); });
+    cuda_check(cudaMemcpy(d + op, params, 8 * sizeof(double) * n_params, cudaMemcpyHostToDevice), "H2D");
+    cuda_check(cudaMemcpy(d + oi, idx, sizeof(int32_t) * n, cudaMemcpyHostToDevice), "H2D");
+    cuda_check(cudaMemcpy(d + ob, b, sizeof(int32_t) * n, cudaMemcpyHostToDevice), "H2D");
+    cuda_check(cudaMemcpy(d + os, s, sizeof(int32_t) * n, cudaMemcpyHostToDevice), "H2D");
+    const int rc = nx_perf_eval_dev(reinterpret_cast<double*>(d + op), n_params,
+                                    reinterpret_cast<int32_t*>(d + oi), reinterpret_cast<int32_t*>(d + ob),
+                                    reinterpret_cast<int32_t*>(d + os), reinterpret_cast<double*>(d + oT),
+                                    out_thr ? reinterpret_cast<double*>(d + oh) : nullptr, n, mode, nullptr);
+    if (rc) throw NxError(rc, g_err);
+    cuda_check(cudaMemcpy(out_T, d + oT, sizeof(double) * n, cudaMemcpyDeviceToHost), "D2H");
+    if (out_thr) cuda_check(cudaMemcpy(out_thr, d + oh, sizeof(double) * n, cudaMemcpyDeviceToHost), "D2H");
+  });
+}
+
+// ---- host utilities -------------------------------------------------------------
+int nx_synth_generate(const char* scenario, int64_t n, uint64_t seed, int64_t* prompts,
+                      int64_t* outputs, char* session_ids16) {
+  return guard([&] {
+    const auto rows = nx::synth_rows(nx::scenario_named(scenario), n, seed);
+    for (int64_t i = 0; i < n; ++i) {
+      prompts[i] = rows[i].prompt;
+      outputs[i] = rows[i].output;
+      std::snprintf(session_ids16 + 16 * i, 16, "%s", rows[i].session.c_str());
+    }
+  });
+}
+
+}  // extern "C"

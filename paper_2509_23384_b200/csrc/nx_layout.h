@@ -1,0 +1,99 @@
+// Host/device shared layout of the replica batch in HBM.
+//
+// One replica = one independent servesim::Simulation (proj/src/sim.cpp:57-99).
+// A batch of replicas is packed into structure-of-arrays pools; every per-engine
+// and per-replica region is addressed by element offsets stored in the
+// descriptors below. Plain C layout: compiled by both g++ and nvcc.
+#pragma once
+#include <stdint.h>
+
+#define NX_MAX_ENGINES 32      /* one lane per engine in the warp-wide scans */
+#define NX_TW_CAP 200          /* TradeoffEstimator::kWindow, proj/include/servesim/lens.h:145 */
+
+/* Per-engine static description + pool offsets (one per engine, all replicas). */
+typedef struct NxEngineDesc {
+  double tp[8];            /* ground-truth PerfParams (engine.h:29) */
+  double noise_sigma;
+  double static_w;         /* router static weight for this engine (router.h:42) */
+  int64_t period_us;       /* to_us(state_report_period_ms) */
+  int64_t stale_us;        /* to_us(state_staleness_ms) */
+  uint64_t rng[4];         /* xoshiro state for substream "engine-noise"/engine_id */
+  int64_t wq_off;          /* wait-queue pool, capacity = replica n_req */
+  int64_t rq_off;          /* run-queue pool, capacity = replica n_req */
+  int64_t plan_off;        /* in-flight plan allocations, capacity = replica n_req */
+  int64_t cache_off;       /* prefix-cache LRU arrays, capacity = replica n_sess */
+  int64_t ring_off;        /* learner ring, capacity = long_window */
+  int64_t tw_off;          /* tradeoff window, capacity = NX_TW_CAP */
+  int64_t dq_off;          /* report deliveries FIFO, capacity = dq_cap */
+  int64_t lat_off;         /* latency_based rolling window, capacity = lat_cap */
+  int32_t engine_id, policy;
+  int32_t kv_blocks, block_size, m_max, q_max, static_budget, wait_cap;
+  int32_t dq_cap, lat_cap;
+} NxEngineDesc;
+
+typedef struct NxReplicaDesc {
+  double ttft_slo, tpot_slo, eps_ratio, q_ref;
+  double alpha, beta, l_bar, td_min;          /* TradeoffModel init */
+  double weights[4], beta_aff, knee, scale_ms, load_half, headroom;
+  double stale_limit, lat_window;
+  uint64_t router_rng[4];
+  int64_t duration_us;
+  int64_t req_off;         /* request pools */
+  int64_t sess_off;        /* router session map */
+  int64_t scratch_off;     /* learner scratch, capacity = long_window doubles */
+  int32_t n_eng, eng_base, n_req, n_sess;
+  int32_t n_iters, route_policy;
+  int32_t long_w, short_w, s_period, l_period, min_s;
+  int32_t pad_;
+} NxReplicaDesc;
+
+/* Per-replica result (device -> host). */
+typedef struct NxReplicaOut {
+  int64_t arrived, rejected, completed, pending, events;
+  uint64_t event_hash;
+  int32_t status;          /* 0 ok, 1 invalid_argument, 2 runtime_error, 3 logic_error */
+  int32_t err_site;        /* NX_SITE_* where the error was raised */
+  int64_t err_info;
+} NxReplicaOut;
+
+typedef struct NxEngineOut {
+  double params[8];        /* learner's current PerfParams */
+  int64_t samples;         /* OnlineLearner::samples_seen */
+  int64_t counters[7];     /* LearnerCounters order (learner.h:26-34) */
+  int64_t tradeoff_degenerate;
+  double alpha, beta, l_bar;
+} NxEngineOut;
+
+/* Device pools (all pointers are device pointers). */
+typedef struct NxPools {
+  /* request inputs */
+  const int64_t* arr_us; const double* arr_ms;
+  const int32_t* prompt; const int32_t* target; const int32_t* session;
+  /* request state / outputs */
+  int32_t* prefilled; int32_t* decoded; int64_t* first_us; int64_t* done_us;
+  int32_t* req_engine; uint8_t* kv_admitted;
+  /* queues and plans */
+  int32_t* wq; int32_t* rq; int32_t* plan_req; int32_t* plan_tok;
+  int32_t* c_tokens; int32_t* c_prev; int32_t* c_next;
+  int32_t* ring_b; int32_t* ring_s; double* ring_y;
+  double* tw_ttft; double* tw_tpot;
+  int64_t* dq_t; uint32_t* dq_seq; double* dq_sv; int64_t* dq_qlen;  /* dq_sv: 5 doubles per entry */
+  double* lat_t; double* lat_e2e;
+  int32_t* sess_engine;
+  int32_t* records;
+  double* scratch;
+  /* descriptors + outputs */
+  const NxReplicaDesc* rep; const NxEngineDesc* eng;
+  NxReplicaOut* rep_out; NxEngineOut* eng_out;
+} NxPools;
+
+enum {
+  NX_SITE_NONE = 0,
+  NX_SITE_BISECT = 1,        /* binary_search_budget invalid inputs (lens.cpp:36-38) */
+  NX_SITE_ALLOCATE = 2,      /* allocate_tokens budget below queue needs (lens.cpp:61-63) */
+  NX_SITE_PREFILL_CAP = 3,   /* prefill_priority prompt exceeds m_max (engine.cpp:74-79) */
+  NX_SITE_SAMPLE = 4,        /* invalid LatencySample (learner.cpp:131-133) */
+  NX_SITE_CAPACITY = 5,      /* score_capacity demand < 1 (router.cpp:54-56) */
+  NX_SITE_OVERFLOW = 6,      /* device capacity exceeded (plan/delivery/latency ring) */
+  NX_SITE_PARAMS = 7         /* predict_latency on invalid params (perf_model.cpp:26-28) */
+};

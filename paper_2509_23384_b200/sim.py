@@ -1,0 +1,196 @@
+"""Reference-facing simulation API (mirror of proj/include/servesim/sim.h).
+
+``run_simulation``, ``sweep`` and the batched ``run_replicas`` take RunConfig
+JSON documents in the reference's schema and return results shaped like
+servesim::RunResult / SweepResult. All replicas of a call run in ONE launch of
+the device lockstep kernel (one warp per replica); the host only parses
+configs, synthesises workloads with the reference's generator semantics and
+formats summaries.
+"""
+from __future__ import annotations
+
+import copy
+import ctypes as C
+import json
+import os
+from dataclasses import dataclass, field
+
+from . import _lib
+from ._lib import RequestRecord, ReplicaSummary, check, lib
+
+
+@dataclass
+class RunResult:  # servesim::RunResult (sim.h:62-73)
+    arrived: int
+    completed: int
+    rejected: int
+    unfinished: int
+    arrival_hash: int
+    event_hash: int
+    decisions: int
+    events: int
+    summary_json: str
+    records: list = field(default_factory=list)
+    learners: list = field(default_factory=list)   # (params8, samples, counters7) per engine
+
+    @property
+    def summary(self) -> dict:
+        return json.loads(self.summary_json)
+
+
+def _texts(cfgs):
+    return [c if isinstance(c, str) else json.dumps(c) for c in cfgs]
+
+
+class Batch:
+    """One device batch of replicas (an nx_sim handle)."""
+
+    def __init__(self, cfgs, device: int = 0, host_threads: int | None = None):
+        texts = _texts(cfgs)
+        arr = (C.c_char_p * len(texts))(*[t.encode() for t in texts])
+        h = C.c_void_p()
+        threads = host_threads or max(1, os.cpu_count() or 1)
+        check(lib().nx_sim_create_json(arr, len(texts), device, threads, C.byref(h)))
+        self.h = h
+        self.n = len(texts)
+
+    def upload(self):
+        check(lib().nx_sim_upload(self.h))
+
+    def launch(self):
+        check(lib().nx_sim_launch(self.h))
+
+    def download(self):
+        check(lib().nx_sim_download(self.h))
+
+    def synchronize(self):
+        check(lib().nx_sim_synchronize(self.h))
+
+    def run(self):
+        check(lib().nx_sim_run(self.h))
+        return self
+
+    def kernel_ms(self) -> float:
+        v = C.c_float()
+        check(lib().nx_sim_last_kernel_ms(self.h, C.byref(v)))
+        return v.value
+
+    def io_bytes(self):
+        a, b = C.c_int64(), C.c_int64()
+        check(lib().nx_sim_io_bytes(self.h, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
+    def summaries(self):
+        out = (ReplicaSummary * self.n)()
+        check(lib().nx_sim_summaries(self.h, out))
+        return list(out)
+
+    def summary_json(self, r: int) -> str:
+        n = C.c_int64()
+        check(lib().nx_sim_summary_json(self.h, r, None, 0, C.byref(n)))
+        buf = C.create_string_buffer(n.value + 1)
+        check(lib().nx_sim_summary_json(self.h, r, buf, n.value + 1, C.byref(n)))
+        return buf.value.decode()
+
+    def records(self, r: int):
+        n = C.c_int64()
+        check(lib().nx_sim_records(self.h, r, None, 0, C.byref(n)))
+        arr = (RequestRecord * max(1, n.value))()
+        check(lib().nx_sim_records(self.h, r, arr, n.value, C.byref(n)))
+        return list(arr)[: n.value]
+
+    def learner(self, r: int, e: int):
+        p = (C.c_double * 8)()
+        s = C.c_int64()
+        cnt = (C.c_int64 * 7)()
+        check(lib().nx_sim_learner(self.h, r, e, p, C.byref(s), cnt))
+        return list(p), s.value, list(cnt)
+
+    def result(self, r: int, with_records: bool = True, n_engines: int | None = None) -> RunResult:
+        s = self.summaries()[r]
+        if s.status != 0:
+            _raise_status(s)
+        sj = self.summary_json(r)
+        ne = n_engines if n_engines is not None else len(json.loads(sj)["learners"])
+        return RunResult(s.arrived, s.completed, s.rejected, s.unfinished, s.arrival_hash,
+                         s.event_hash, s.decisions, s.events, sj,
+                         self.records(r) if with_records else [],
+                         [self.learner(r, e) for e in range(ne)])
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().nx_sim_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _raise_status(s):
+    msg = f"device replica failed at site {s.err_site}"
+    if s.status == _lib.NX_EINVAL:
+        raise ValueError(msg)
+    if s.status == _lib.NX_ELOGIC:
+        raise _lib.LogicError(msg)
+    raise RuntimeError(msg)
+
+
+def run_replicas(cfgs, device: int = 0, with_records: bool = False):
+    b = Batch(cfgs, device).run()
+    try:
+        return [b.result(r, with_records) for r in range(b.n)]
+    finally:
+        b.close()
+
+
+def run_simulation(cfg, device: int = 0) -> RunResult:
+    """servesim::run_simulation (sim.cpp:596-599) on the device."""
+    return run_replicas([cfg], device, with_records=True)[0]
+
+
+def sweep(base: dict, axis: str, values, device: int = 0):
+    """servesim::sweep (sim.cpp:608-642): every value becomes one replica of a
+    single device batch instead of a sequential loop. Per-value failures are
+    reported per row, like the reference."""
+    if axis not in ("rate", "policy", "budget"):
+        raise RuntimeError(f"unknown sweep axis: {axis}")
+    cfgs = []
+    for v in values:
+        c = copy.deepcopy(base)
+        c.setdefault("output", {})["dir"] = ""
+        if axis == "rate":
+            c.setdefault("workload", {})["mode"] = "qps"
+            c["workload"]["rate"] = float(v)
+        elif axis == "policy":
+            for e in c["engines"]:
+                e["scheduler_policy"] = v
+        else:
+            for e in c["engines"]:
+                e["static_budget"] = int(v)
+        cfgs.append(c)
+    rows = []
+    b = Batch(cfgs, device).run()
+    try:
+        sums = b.summaries()
+        for i, v in enumerate(values):
+            if sums[i].status != 0:
+                rows.append({"value": str(v), "ok": False, "error": f"site {sums[i].err_site}"})
+            else:
+                rows.append({"value": str(v), "ok": True, "result": b.result(i, False)})
+    finally:
+        b.close()
+    return {"axis": axis, "rows": rows}
+
+
+def synth_generate(scenario: str, n: int, seed: int):
+    """workload.cpp:137-166 semantics -> (prompts, outputs, session_ids)."""
+    P = (C.c_int64 * n)()
+    O = (C.c_int64 * n)()
+    S = C.create_string_buffer(16 * n)
+    check(lib().nx_synth_generate(scenario.encode(), n, seed, P, O, S))
+    raw = S.raw
+    sess = [raw[16 * i:16 * i + 16].split(b"\0", 1)[0].decode() for i in range(n)]
+    return list(P), list(O), sess

@@ -1,0 +1,363 @@
+#!/usr/bin/env python3
+"""NexusSched hot-path benchmark: scheduling decisions/s (routes + batches).
+
+Workload (BASELINE.json config 5): the arrival-rate x seed x router-policy
+sweep of 8-engine heterogeneous LENS+PRISM replicas (2000 sharegpt requests
+each). Replicas are independent, so every GPU owns a fixed shard of
+`--replicas-per-gpu` (default 512) replicas of the interleaved 4096-replica
+grid — rank k runs grid rows [k*R, (k+1)*R) — and N GPUs run N*R replicas
+("scaling": "weak"; N=8 is exactly the 4096-replica sweep). One step = one
+launch of the device lockstep kernel over the rank's whole shard, inputs
+resident in HBM. The single collective is the end-of-run NCCL all-gather of
+per-replica summaries (K6).
+
+  value : decisions / device time of the K timed launches (max over ranks)
+  e2e   : same metric through the C-ABI with host buffers each step
+          (pinned H2D of the traces + descriptors, launch, D2H of results)
+  --impl reference : the reference C++ simulator (oracle/_ref, compiled
+          unmodified from /root/reference/proj/src) on the host cores, same
+          workload, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "scheduling decisions/sec (routes+batches) at 1/2/4/8 B200; % HBM roofline"
+UNIT = "decisions/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["nx", "reference"], default="nx")
+    ap.add_argument("--replicas-per-gpu", type=int, default=512)
+    ap.add_argument("--requests", type=int, default=2000)
+    ap.add_argument("--cpu-sample", type=int, default=32, help="replicas timed for cpu_baseline")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def shard_configs(rank: int, per_gpu: int, n_req: int):
+    from paper_2509_23384_b200 import workloads as W
+    total = per_gpu * (rank + 1)
+    grid = W.sweep_configs(n_replicas=min(4096, max(total, 1)), n=n_req)
+    if total > len(grid):  # beyond the 4096 grid: extend with further seeds
+        extra = []
+        seed = 65
+        while len(grid) + len(extra) < total:
+            for rate in W.SWEEP_RATES:
+                for pol in W.SWEEP_POLICIES:
+                    extra.append(W.sweep_replica(rate, seed, pol, n_req))
+            seed += 1
+        grid = grid + extra
+    return grid[rank * per_gpu:(rank + 1) * per_gpu]
+
+
+def workload_desc(per_gpu: int, n_req: int, n_gpus: int) -> dict:
+    return {
+        "workload": (f"config5 sweep shard: {per_gpu} replicas/GPU of the rate x seed x policy grid "
+                     f"(16 rates 10..47.5 req/s x 4 router policies prism/round_robin/least_loaded/"
+                     f"latency_based x seeds), 8 heterogeneous engines (2 fast/3 medium/3 slow), "
+                     f"LENS scheduler + online learner, {n_req} sharegpt requests per replica"),
+        "replicas_per_gpu": per_gpu,
+        "replicas_total": per_gpu * n_gpus,
+        "requests_per_replica": n_req,
+        "l2": "flushed between timed steps (256 MiB device write)",
+        "parallelism": f"replica-sharded dp{n_gpus}",
+    }
+
+
+# ---------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > i + 2 and s[i + 2].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------------- roofline
+def algorithmic_bytes(batch, n_rep: int, n_eng: int = 8) -> int:
+    """SURVEY.md §8(d) compulsory bytes, from the device work counters."""
+    total = 0
+    sums = batch.summaries()
+    for r in range(n_rep):
+        w = batch.work(r)
+        steps, sum_b, win, lin, struct = w[0], w[1], w[2], w[3], w[4]
+        total += sums[r].arrived * (48 * n_eng + 36)       # K3 per route
+        total += steps * (96 + 24) + 4 * win + 8 * sum_b     # K2 per batch decision
+        total += 32 * sum_b + steps * (64 + 32)              # K5 per executed step
+        total += 16 * lin + 16 * struct                      # K4 refits (window reads)
+    return total
+
+
+def peaks():
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text()), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+def k1_model_eval(torch, dev) -> dict:
+    """K1 perf-model evaluator on 2^26 streamed records (HBM-bound)."""
+    from paper_2509_23384_b200 import perf_model
+    n = 1 << 26
+    g = torch.Generator(device=dev).manual_seed(5)
+    params = perf_model.profile_table(dev)          # fast/medium/slow + priors
+    idx = torch.randint(0, params.shape[0], (n,), device=dev, dtype=torch.int32, generator=g)
+    b = torch.randint(1, 257, (n,), device=dev, dtype=torch.int32, generator=g)
+    s = b + torch.randint(0, 8192, (n,), device=dev, dtype=torch.int32, generator=g)
+    out = torch.empty(n, device=dev, dtype=torch.float64)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    times = []
+    for it in range(8):
+        flush.fill_(it & 0xff)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        perf_model.eval_device(params, idx, b, s, out, None, stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        if it >= 3:
+            times.append(e0.elapsed_time(e1) / 1e3)
+    t = statistics.mean(times)
+    byts = n * (4 + 4 + 4 + 8)
+    pk, src = peaks()
+    return {"kernel": "perf_eval_kernel (K1, fp64 deterministic)", "records": n,
+            "records_per_s": n / t, "ms": t * 1e3,
+            "roofline": {"bound": "hbm", "achieved": byts / t / 1e9, "peak": pk["hbm_gbs"],
+                         "unit": "GB/s", "frac": byts / t / 1e9 / pk["hbm_gbs"],
+                         "traffic": None, "peak_source": src,
+                         "bytes_per_record": 20}}
+
+
+# ---------------------------------------------------------------------------- arms
+def cpu_reference_rate(cfgs, threads: int):
+    sys.path.insert(0, str(ROOT / "tests"))
+    from oracle_lib import Port, Ref, ref_available
+    checker = Ref() if ref_available() else Port()
+    kind = "reference" if ref_available() else "port"
+    dec, _, wall = checker.run_batch(cfgs, threads)
+    return sum(dec) / wall, kind, wall, sum(dec)
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    cfgs = shard_configs(0, args.replicas_per_gpu, args.requests)
+    sample = cfgs[: max(threads, min(len(cfgs), threads))]
+    rates = []
+    for i in range(args.warmup + args.steps):
+        r, kind, wall, dec = cpu_reference_rate(sample, threads)
+        if i >= args.warmup:
+            rates.append((r, wall, dec))
+    tot_dec = sum(x[2] for x in rates)
+    tot_wall = sum(x[1] for x in rates)
+    value = tot_dec / tot_wall
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": tot_wall / args.steps * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_desc(args.replicas_per_gpu, args.requests, args.gpus),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
+                         "sample": f"{len(sample)} replicas of the rank-0 shard per step, "
+                                   f"one std::thread per host core"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_nx(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2509_23384_b200 import sim
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    def max_over_ranks(v: float) -> float:
+        if world == 1:
+            return v
+        t = torch.tensor([v], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(v: float) -> float:
+        if world == 1:
+            return v
+        t = torch.tensor([v], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    cfgs = shard_configs(rank, args.replicas_per_gpu, args.requests)
+    batch = sim.Batch(cfgs, device=local, host_threads=os.cpu_count())
+    batch.upload()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    for i in range(args.warmup):
+        batch.launch()
+        batch.synchronize()
+    batch.download()
+    batch.synchronize()
+    sums = batch.summaries()
+    bad = [i for i, s in enumerate(sums) if s.status != 0]
+    if bad:
+        raise RuntimeError(f"rank {rank}: {len(bad)} replicas failed (first site {sums[bad[0]].err_site})")
+    decisions_step = sum(s.decisions for s in sums)
+
+    barrier()
+    kernel_s = 0.0
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.fill_(i & 0xff)
+            torch.cuda.synchronize(dev)
+            batch.launch()
+            batch.synchronize()
+            kernel_s += batch.kernel_ms() / 1e3
+    barrier()
+    t_dev = max_over_ranks(kernel_s)
+    total_dec = sum_over_ranks(decisions_step * args.steps)
+    value = total_dec / t_dev
+
+    # e2e through the C-ABI with host buffers (upload + launch + download)
+    e2e = None
+    if not args.no_e2e:
+        barrier()
+        t0 = time.perf_counter()
+        for i in range(args.steps):
+            batch.run()
+        wall = time.perf_counter() - t0
+        barrier()
+        h2d, d2h = batch.io_bytes()
+        e2e_t = max_over_ranks(wall)
+        e2e = {"value": total_dec / e2e_t, "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h}
+
+    # K6: one NCCL all-gather of the per-replica summaries (the only exchange)
+    gathered = None
+    if world > 1:
+        nbytes = batch.summaries_nbytes()
+        buf = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+        batch.copy_summaries(buf.data_ptr())
+        out = torch.empty(nbytes * world, dtype=torch.uint8, device=dev)
+        dist.all_gather_into_tensor(out, buf)
+        torch.cuda.synchronize(dev)
+        gathered = world * len(cfgs)
+
+    # roofline of the dominant kernel (nx_sim_kernel), from device work counters
+    pk, src = peaks()
+    alg = algorithmic_bytes(batch, len(cfgs))
+    per_launch_s = kernel_s / args.steps
+    achieved = alg / per_launch_s / 1e9
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": t_dev / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_desc(args.replicas_per_gpu, args.requests, world),
+            "decisions_per_step": total_dec / args.steps,
+            "gpu_launches": args.steps,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                         "frac": achieved / pk["hbm_gbs"], "traffic": None,
+                         "kernel": "nx_sim_kernel", "peak_source": src,
+                         "algorithmic_bytes_per_launch": alg},
+            "clocks": clk.summary(),
+        }
+        if e2e:
+            line["e2e"] = e2e
+        if gathered is not None:
+            line["gathered_summaries"] = gathered
+        try:
+            line["model_eval"] = k1_model_eval(torch, dev)
+        except Exception as exc:  # keep the headline line even if K1 fails
+            line["model_eval"] = {"error": repr(exc)}
+        if world == 1 and not args.no_cpu_baseline:
+            sample = cfgs[: args.cpu_sample]
+            rate, kind, wall, dec = cpu_reference_rate(sample, os.cpu_count() or 1)
+            line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": os.cpu_count(),
+                                    "kind": kind,
+                                    "sample": f"{len(sample)} replicas of this shard, "
+                                              f"{dec} decisions in {wall:.1f} s"}
+        print(json.dumps(line), flush=True)
+    batch.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_nx(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -95,6 +95,15 @@ int nx_sim_summaries(nx_sim_t h, nx_replica_summary* out);
 int nx_sim_summary_json(nx_sim_t h, int32_t replica, char* buf, int64_t cap, int64_t* len);
 int nx_sim_records(nx_sim_t h, int32_t replica, nx_request_record* out, int64_t cap,
                    int64_t* n);
+/* Work counters of a replica (roofline accounting): [0] executed steps,
+ * [1] sum of batch sizes, [2] LENS candidate-window waiters scanned,
+ * [3] linear-refit window samples, [4] structural-refit window samples,
+ * [5] gauged (profiled) fits. */
+int nx_sim_work(nx_sim_t h, int32_t replica, int64_t* out6);
+/* SM cycles per phase of a replica (lane-0 clock64): [0] event selection +
+ * hash, [1] routing + admission, [2] step planning, [3] step completion,
+ * [4] state reports, [5] linear refits, [6] structural refits, [7] deliveries */
+int nx_sim_phase_cycles(nx_sim_t h, int32_t replica, int64_t* out8);
 /* Learner state per engine: params[8] + samples + counters[7]. */
 int nx_sim_learner(nx_sim_t h, int32_t replica, int32_t engine, double* params8,
                    int64_t* samples, int64_t* counters7);
@@ -105,6 +114,9 @@ void nx_sim_destroy(nx_sim_t h);
  * GPUs (one collective per run; no per-step exchange). Device pointer to the
  * handle's summaries, filled by nx_sim_launch, for an NCCL all-gather. */
 int nx_sim_summaries_dev(nx_sim_t h, void** dev_ptr, int64_t* bytes);
+/* Device-to-device copy of those summaries into a caller buffer (e.g. the
+ * send buffer of an ncclAllGather); ordered on the handle's stream. */
+int nx_sim_copy_summaries(nx_sim_t h, void* dst_dev);
 
 /* ---- host utilities (reference workload generator semantics) -------------
  * synth_generate (proj/src/workload.cpp:137-166): prompts/outputs/session

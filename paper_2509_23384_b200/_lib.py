@@ -64,6 +64,9 @@ def lib() -> C.CDLL:
                                  _P(C.c_int64)]
     L.nx_sim_destroy.argtypes = [C.c_void_p]
     L.nx_sim_destroy.restype = None
+    L.nx_sim_work.argtypes = [C.c_void_p, C.c_int32, _P(C.c_int64)]
+    L.nx_sim_phase_cycles.argtypes = [C.c_void_p, C.c_int32, _P(C.c_int64)]
+    L.nx_sim_copy_summaries.argtypes = [C.c_void_p, C.c_void_p]
     L.nx_sim_summaries_dev.argtypes = [C.c_void_p, _P(C.c_void_p), _P(C.c_int64)]
     L.nx_perf_eval_dev.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
                                    C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p]

@@ -15,7 +15,6 @@
 
 namespace nxd {
 
-constexpr double kCertMargin = 1e-9;  // >> 2*(n-1)*2^-53 for n <= 2^20
 
 // ---- 5x5 elimination (learner.cpp:24-60), fully unrolled in registers -----
 __device__ __forceinline__ double dmax(double m, double v) { return (m < v) ? v : m; }
@@ -139,7 +138,10 @@ struct Window {
   const int32_t* rs;
   const double* ry;
   int size, head, n;
-  __device__ __forceinline__ int slot(int i) const { return (head + size - n + i) % size; }
+  __device__ __forceinline__ int slot(int i) const {
+    const int k = head + size - n + i;  // < 2 * size
+    return k >= size ? k - size : k;
+  }
 };
 
 __device__ __forceinline__ Window window_of(const Ctx& c, int e, int n_want) {
@@ -162,7 +164,8 @@ __device__ bool update_linear(Ctx& c, int e) {
   const int n = w.n;
   if (n < 5) return false;
   const Params cur = g.lp;
-  double* rows = c.scratch + c.d->long_w + kFbTable;  // (1/thr, s/thr) per sample
+  if (c.lane == 0) c.rs->work[3] += n;
+  double* rows = c.scratch + 6 * c.d->long_w + kFbTable;  // (1/thr, s/thr) per sample
   double acc = 0.0;
   for (int base = 0; base < n; base += 32) {
     const int i = base + c.lane;
@@ -309,144 +312,347 @@ __device__ bool update_linear(Ctx& c, int e) {
 }
 
 // ---- structural tier (learner.cpp:209-298, 346-440) --------------------------
+//
+// One structural update evaluates ~76 profiled fits (learner.cpp:373-430) over
+// the same <= long_window samples. Per update the window is staged once in
+// chronological order (b, s, y, 1/y); per fit only the (kB, kS)-dependent
+// quantities are rebuilt: a 1/f_B table over batch sizes and a per-sample
+// 1/f_S cache, reused while kS is unchanged (every other coordinate move).
+// The scaled design row is r = (1, 1/f, s/f, b, s) / y, so of the 15 unique
+// A^T A entries and 5 A^T b entries, the 9 + 3 built only from {1, b, s}/y are
+// fit-invariant and accumulated once per update; each fit accumulates the
+// other 11 in one pass.
+//
+// Both squared-error sums a fit needs have closed forms in those normal
+// equations — with the target y = 1 after 1/y weighting,
+//   SSE(x) = y2 - 2 x.t + x^T A x
+// — for the ridge scale (sse(x), learner.cpp:251-260) and for the windowed
+// SSE of the clamped fit (windowed_sse(p), :209-222; T(p) is exactly x'.row
+// for x' = (tau0, a, c, tauB, tauS)). Each closed form carries an explicit
+// rounding-error bound; any decision inside the bound is re-taken on the
+// reference's direct left-fold evaluation (wsse_exact / sse_x_exact).
 
-// windowed_sse (learner.cpp:209-222) with direct model evaluation.
-__device__ double wsse_tree(Ctx& c, const Window& w, const Params& p) {
+constexpr double kU = 1.1102230246251565e-16;  // 2^-53
+
+// Replica scratch layout (doubles), W = long_window:
+//   [0,W) b  [W,2W) s  [2W,3W) y  [3W,5W) packed {1/y, b | s<<32} records
+//   [5W,6W) 1/f_S per sample (only when s exceeds the token-count table)
+//   [6W, 6W+1024) 1/f_B by batch size   [6W+1024, 8W+1024) linear-tier rows
+//   [8W+1024, 9W+1024) distinct token counts (int32)
+//   [9W+1024, 9W+1024+kSTab) 1/f_S by token count
+constexpr int kSTab = 10240;  // token-count table (bitmap fits the 1280 B stage)
+
+struct Stage {          // chronological window staged in the replica scratch
+  const double* sb;     // b
+  const double* ss;     // s
+  const double* sy;     // observed_ms
+  const double2* rec;   // {1 / observed_ms, b | s << 32}: one 16-byte load per sample
+  double* ifs;          // 1 / f_S(s_i) for kS == ifs_k (when s exceeds the table)
+  double* ifb;          // 1 / f_B(b) for kB == ifb_k, b in [1, tab]
+  int* us;              // distinct s values of the window
+  double* stab;         // 1 / f_S(s) for s in us, kS == ifs_k
+  int n, tab, U;
+  bool use_tab;
+  double ifs_k, ifb_k;
+  // fit-invariant normal-equation entries: A00 A03 A04 A33 A34 A44, t0 t3 t4
+  double A00, A03, A04, A33, A34, A44, t0, t3, t4;
+};
+
+__device__ __forceinline__ Stage stage_of(const Ctx& c) {
+  const int W = c.d->long_w;
+  Stage s;
+  s.sb = c.scratch;
+  s.ss = c.scratch + W;
+  s.sy = c.scratch + 2 * W;
+  s.rec = reinterpret_cast<const double2*>(c.scratch + 3 * W);
+  s.ifs = c.scratch + 5 * W;
+  s.ifb = c.scratch + 6 * W;
+  s.us = reinterpret_cast<int*>(c.scratch + 8 * W + kFbTable);
+  s.stab = c.scratch + 9 * W + kFbTable;
+  s.n = 0;
+  s.tab = 0;
+  s.U = 0;
+  s.use_tab = false;
+  s.ifs_k = -1.0;
+  s.ifb_k = -1.0;
+  return s;
+}
+
+// windowed_sse (learner.cpp:209-222), direct model evaluation, tree order
+__device__ double wsse_tree(Ctx& c, const Stage& S, const Params& p) {
   double part = 0.0;
-  for (int i = c.lane; i < w.n; i += 32) {
-    const int k = w.slot(i);
-    const double y = w.ry[k];
-    const double r = (y - predict(p, w.rb[k], w.rs[k])) / y;
+  for (int i = c.lane; i < S.n; i += 32) {
+    const double y = S.sy[i];
+    const double r = (y - predict(p, S.sb[i], S.ss[i])) / y;
     part += r * r;
   }
   return warp_sum(part);
 }
-__device__ double wsse_exact(Ctx& c, const Window& w, const Params& p) {
+// the same sum in the reference's left-to-right order
+__device__ double wsse_exact(Ctx& c, const Stage& S, const Params& p) {
   double run = 0.0;
-  for (int base = 0; base < w.n; base += 32) {
+  for (int base = 0; base < S.n; base += 32) {
     const int i = base + c.lane;
     double rr = 0.0;
-    if (i < w.n) {
-      const int k = w.slot(i);
-      const double y = w.ry[k];
-      const double r = (y - predict(p, w.rb[k], w.rs[k])) / y;
+    if (i < S.n) {
+      const double y = S.sy[i];
+      const double r = (y - predict(p, S.sb[i], S.ss[i])) / y;
       rr = r * r;
     }
-    fold_exact_chunk(c, rr, min(32, w.n - base), run);
+    fold_exact_chunk(c, rr, min(32, S.n - base), run);
+  }
+  return __shfl_sync(NX_FULL, run, 0);
+}
+// gauged_fit's ridge-scale sse(x) exactly as the reference forms it
+// (rows (1, 1/f, s/f, b, s), f = max(fB fS, 1e-300); learner.cpp:234-260)
+__device__ double sse_x_exact(Ctx& c, const Stage& S, double kB, double kS, const double x[5]) {
+  double run = 0.0;
+  for (int base = 0; base < S.n; base += 32) {
+    const int i = base + c.lane;
+    double rr = 0.0;
+    if (i < S.n) {
+      const double b = S.sb[i], s = S.ss[i], y = S.sy[i];
+      double f = raw_factor(kB, b) * raw_factor(kS, s);
+      f = (f < 1e-300) ? 1e-300 : f;
+      double pred = 0.0;
+      pred += 1.0 * x[0];
+      pred += (1.0 / f) * x[1];
+      pred += (s / f) * x[2];
+      pred += b * x[3];
+      pred += s * x[4];
+      const double r = (y - pred) / y;
+      rr = r * r;
+    }
+    fold_exact_chunk(c, rr, min(32, S.n - base), run);
   }
   return __shfl_sync(NX_FULL, run, 0);
 }
 
-// Certified "a < b * f" between two windowed SSE values whose tree sums are
-// a_t, b_t; falls back to exact folds when the tree cannot decide.
-__device__ bool less_scaled(Ctx& c, const Window& w, double a_t, const Params& pa, double b_t,
-                            const Params& pb, double f) {
-  const double rhs = b_t * f;
-  if (a_t < rhs * (1.0 - kCertMargin)) return true;
-  if (a_t > rhs * (1.0 + kCertMargin)) return false;
-  const double a = wsse_exact(c, w, pa);
-  const double b = wsse_exact(c, w, pb);
-  return a < b * f;
+struct Normal {  // assembled normal equations of one fit
+  double A[5][5], t[5], y2;
+};
+
+// SSE(x) = y2 - 2 x.t + x^T A x with its absolute rounding bound: accumulation
+// error of every entry (all terms positive) plus the closed-form arithmetic,
+// plus the per-term gap between x.row and the reference's model evaluation.
+__device__ void closed_sse(const Normal& N, const double x[5], int n, double& val, double& bound) {
+  double lin = 0.0, lin_abs = 0.0, quad = 0.0, quad_abs = 0.0;
+#pragma unroll
+  for (int i = 0; i < 5; ++i) {
+    lin += x[i] * N.t[i];
+    lin_abs += fabs(x[i]) * N.t[i];
+#pragma unroll
+    for (int j = 0; j < 5; ++j) {
+      quad += x[i] * x[j] * N.A[i][j];
+      quad_abs += fabs(x[i]) * fabs(x[j]) * N.A[i][j];
+    }
+  }
+  val = N.y2 - 2.0 * lin + quad;
+  const double M = N.y2 + 2.0 * lin_abs + quad_abs;
+  const double s = val > 0.0 ? val : 0.0;
+  bound = 2.0 * (static_cast<double>(n) + 64.0) * kU * M +
+          32.0 * kU * (sqrt(static_cast<double>(n) * (s + 1.0)) + s) + 1e-300;
+}
+
+// Per-update staging: chronological copy, gate statistics, invariant sums.
+__device__ void stage_window(Ctx& c, const Window& w, const Params& cur, Stage& S, bool& saturated,
+                             int& shaped, int& bmax) {
+  double* sb = const_cast<double*>(S.sb);
+  double* ss = const_cast<double*>(S.ss);
+  double* sy = const_cast<double*>(S.sy);
+  double2* rec = const_cast<double2*>(S.rec);
+  S.n = w.n;
+  bool unsat = false;
+  int shp = 0, bm = 1, smx = 1;
+  double a00 = 0, a03 = 0, a04 = 0, a33 = 0, a34 = 0, a44 = 0, t0 = 0, t3 = 0, t4 = 0;
+  for (int i = c.lane; i < w.n; i += 32) {
+    const int k = w.slot(i);
+    const int bi = w.rb[k], si = w.rs[k];
+    const double b = bi, s = si, y = w.ry[k];
+    const double iy = 1.0 / y;
+    sb[i] = b;
+    ss[i] = s;
+    sy[i] = y;
+    rec[i] = make_double2(iy, __longlong_as_double(static_cast<long long>(
+                                  (static_cast<unsigned long long>(si) << 32) | static_cast<unsigned>(bi))));
+    if (cur.kB * b < 20.0 || cur.kS * s < 20.0) unsat = true;
+    if (si >= 64 && si >= 4 * bi) ++shp;
+    bm = max(bm, bi);
+    smx = max(smx, si);
+    const double r3 = b * iy, r4 = s * iy;
+    a00 += iy * iy; a03 += iy * r3; a04 += iy * r4;
+    a33 += r3 * r3; a34 += r3 * r4; a44 += r4 * r4;
+    t0 += iy; t3 += r3; t4 += r4;
+  }
+  saturated = !__any_sync(NX_FULL, unsat);
+  shaped = static_cast<int>(__reduce_add_sync(NX_FULL, static_cast<unsigned>(shp)));
+  bmax = warp_max_int(bm);
+  S.A00 = warp_sum(a00); S.A03 = warp_sum(a03); S.A04 = warp_sum(a04);
+  S.A33 = warp_sum(a33); S.A34 = warp_sum(a34); S.A44 = warp_sum(a44);
+  S.t0 = warp_sum(t0); S.t3 = warp_sum(t3); S.t4 = warp_sum(t4);
+  S.tab = bmax < kFbTable ? bmax : kFbTable - 1;
+  // distinct token counts: a presence bitmap in the shared stage, compacted
+  // into S.us so each new kS costs one expm1 per distinct s, not per sample
+  const int smax = warp_max_int(smx);
+  S.use_tab = smax < kSTab;
+  if (S.use_tab) {
+    uint32_t* bits = reinterpret_cast<uint32_t*>(c.chunk);
+    const int words = (smax >> 5) + 1;
+    __syncwarp();
+    for (int wd = c.lane; wd < words; wd += 32) bits[wd] = 0u;
+    __syncwarp();
+    for (int i = c.lane; i < w.n; i += 32) {
+      const int si = static_cast<int>(ss[i]);
+      atomicOr(&bits[si >> 5], 1u << (si & 31));
+    }
+    __syncwarp();
+    int base = 0;
+    for (int w0 = 0; w0 < words; w0 += 32) {
+      const int wd = w0 + c.lane;
+      unsigned m = wd < words ? bits[wd] : 0u;
+      const int cnt = __popc(m);
+      const int incl = warp_incl_scan(cnt);
+      int off = base + incl - cnt;
+      while (m) {
+        const int bit = __ffs(m) - 1;
+        m &= m - 1;
+        S.us[off++] = wd * 32 + bit;
+      }
+      base += __shfl_sync(NX_FULL, incl, 31);
+    }
+    S.U = base;
+  }
+  __syncwarp();
 }
 
 struct FitOut {
   Params p;
-  double err;  // tree value; +inf when the solve failed
+  double err, bound;  // closed-form windowed SSE and its rounding bound; err=inf on failure
 };
 
 // gauged_fit (learner.cpp:228-298) for fixed (kB, kS).
-__device__ FitOut gauged_fit(Ctx& c, const Window& w, const Params& cur, double kB, double kS,
-                             int bmax) {
-  const int n = w.n;
-  double* fs_cache = c.scratch;
-  double* fbt = c.scratch + c.d->long_w;  // raw batch factors, index b
-  const int tab = bmax < kFbTable ? bmax : kFbTable - 1;
-  __syncwarp();
-  for (int b = 1 + c.lane; b <= tab; b += 32) fbt[b] = raw_factor(kB, static_cast<double>(b));
-  __syncwarp();
-  double acc = 0.0;
-  for (int base = 0; base < n; base += 32) {
-    const int i = base + c.lane;
+__device__ FitOut gauged_fit(Ctx& c, Stage& S, const Params& cur, double kB, double kS) {
+  if (c.lane == 0) c.rs->work[5] += 1;
+  const int n = S.n;
+  if (kB != S.ifb_k) {
     __syncwarp();
-    if (i < n) {
-      const int k = w.slot(i);
-      const int bi = w.rb[k];
-      const double b = bi, s = w.rs[k], y = w.ry[k];
-      const double fb = bi <= tab ? fbt[bi] : raw_factor(kB, b);
-      const double fs = raw_factor(kS, s);
-      fs_cache[i] = fs;
-      double f = fb * fs;
-      f = (f < 1e-300) ? 1e-300 : f;
-      const double iy = 1.0 / y;
-      double* row = c.chunk + c.lane * 5;
-      row[0] = 1.0 * iy;
-      row[1] = (1.0 / f) * iy;
-      row[2] = (s / f) * iy;
-      row[3] = b * iy;
-      row[4] = s * iy;
+    for (int b = 1 + c.lane; b <= S.tab; b += 32)
+      S.ifb[b] = 1.0 / raw_factor(kB, static_cast<double>(b));
+    S.ifb_k = kB;
+    __syncwarp();
+  }
+  const bool new_s = kS != S.ifs_k;
+  if (new_s && S.use_tab) {
+    __syncwarp();
+    for (int k = c.lane; k < S.U; k += 32) {
+      const int sv = S.us[k];
+      S.stab[sv] = 1.0 / raw_factor(kS, static_cast<double>(sv));
     }
     __syncwarp();
-    fold_chunk(c, min(32, n - base), acc);
   }
-  double ata[5][5], atb[5];
-  gather_normal(acc, ata, atb);
-  const double y2 = static_cast<double>(n);
+  double a01 = 0, a02 = 0, a11 = 0, a12 = 0, a22 = 0, a13 = 0, a14 = 0, a23 = 0, a24 = 0;
+  double t1 = 0, t2 = 0;
+  auto accumulate = [&](double iy, int bi, int si, double ifs) {
+    const double b = bi, s = si;
+    const double ifb = bi <= S.tab ? S.ifb[bi] : 1.0 / raw_factor(kB, b);
+    double q = ifb * ifs;  // 1 / max(fB fS, 1e-300)
+    q = q > 1e300 ? 1e300 : q;
+    const double u1 = q * iy, u2 = (s * q) * iy, r3 = b * iy, r4 = s * iy;
+    a01 += iy * u1; a02 += iy * u2; a11 += u1 * u1; a12 += u1 * u2; a22 += u2 * u2;
+    a13 += u1 * r3; a14 += u1 * r4; a23 += u2 * r3; a24 += u2 * r4;
+    t1 += u1; t2 += u2;
+  };
+  if (S.use_tab) {
+    // 4 samples per lane in flight: the record loads and the two table
+    // gathers of a group issue back to back (memory-level parallelism)
+    int i = c.lane;
+    for (; i + 96 < n; i += 128) {
+      double2 r[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) r[u] = S.rec[i + 32 * u];
+      double fs[4];
+      int bi[4], si[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const long long bs = __double_as_longlong(r[u].y);
+        bi[u] = static_cast<int>(bs & 0xffffffffll);
+        si[u] = static_cast<int>(bs >> 32);
+        fs[u] = S.stab[si[u]];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) accumulate(r[u].x, bi[u], si[u], fs[u]);
+    }
+    for (; i < n; i += 32) {
+      const double2 r = S.rec[i];
+      const long long bs = __double_as_longlong(r.y);
+      const int bi = static_cast<int>(bs & 0xffffffffll), si = static_cast<int>(bs >> 32);
+      accumulate(r.x, bi, si, S.stab[si]);
+    }
+  } else {
+    for (int i = c.lane; i < n; i += 32) {
+      const double2 r = S.rec[i];
+      const long long bs = __double_as_longlong(r.y);
+      const int bi = static_cast<int>(bs & 0xffffffffll), si = static_cast<int>(bs >> 32);
+      double ifs;
+      if (new_s) {
+        ifs = 1.0 / raw_factor(kS, static_cast<double>(si));
+        S.ifs[i] = ifs;  // lane-private slot: read back only by this lane
+      } else {
+        ifs = S.ifs[i];
+      }
+      accumulate(r.x, bi, si, ifs);
+    }
+  }
+  S.ifs_k = kS;
+  Normal N;
+  N.A[0][0] = S.A00; N.A[0][3] = N.A[3][0] = S.A03; N.A[0][4] = N.A[4][0] = S.A04;
+  N.A[3][3] = S.A33; N.A[3][4] = N.A[4][3] = S.A34; N.A[4][4] = S.A44;
+  N.A[0][1] = N.A[1][0] = warp_sum(a01);
+  N.A[0][2] = N.A[2][0] = warp_sum(a02);
+  N.A[1][1] = warp_sum(a11);
+  N.A[1][2] = N.A[2][1] = warp_sum(a12);
+  N.A[2][2] = warp_sum(a22);
+  N.A[1][3] = N.A[3][1] = warp_sum(a13);
+  N.A[1][4] = N.A[4][1] = warp_sum(a14);
+  N.A[2][3] = N.A[3][2] = warp_sum(a23);
+  N.A[2][4] = N.A[4][2] = warp_sum(a24);
+  N.t[0] = S.t0; N.t[1] = warp_sum(t1); N.t[2] = warp_sum(t2); N.t[3] = S.t3; N.t[4] = S.t4;
+  N.y2 = static_cast<double>(n);  // sum of 1.0 * 1.0 (learner.cpp:73)
   const double prior[5] = {cur.tau0, cur.w0 / cur.p_max, cur.ws / cur.p_max, cur.tauB, cur.tauS};
   FitOut out;
   out.err = __longlong_as_double(0x7ff0000000000000LL);
+  out.bound = 0.0;
   double x[5];
   {
     double a[5][5], bb[5];
 #pragma unroll
     for (int i = 0; i < 5; ++i) {
-      bb[i] = atb[i];
+      bb[i] = N.t[i];
 #pragma unroll
-      for (int j = 0; j < 5; ++j) a[i][j] = ata[i][j];
+      for (int j = 0; j < 5; ++j) a[i][j] = N.A[i][j];
     }
     if (!solve5(a, bb, x)) return out;
   }
-  // residual of the unweighted rows under x (lambda scale)
-  auto resid = [&](int i) {
-    const int k = w.slot(i);
-    const int bi = w.rb[k];
-    const double b = bi, s = w.rs[k], y = w.ry[k];
-    const double fb = bi <= tab ? fbt[bi] : raw_factor(kB, b);
-    double f = fb * fs_cache[i];
-    f = (f < 1e-300) ? 1e-300 : f;
-    double pred = 0.0;
-    pred += 1.0 * x[0];
-    pred += (1.0 / f) * x[1];
-    pred += (s / f) * x[2];
-    pred += b * x[3];
-    pred += s * x[4];
-    const double r = (y - pred) / y;
-    return r * r;
-  };
-  double part = 0.0;
-  for (int i = c.lane; i < n; i += 32) part += resid(i);
-  const double sse_t = warp_sum(part);
-  const double den = (y2 < 1e-30) ? 1e-30 : y2;
+  // lambda = min(1e-7, sse(x) / max(y2, 1e-30))  (learner.cpp:84-85, cap 1e-7)
+  const double den = (N.y2 < 1e-30) ? 1e-30 : N.y2;
+  double sv, sb;
+  closed_sse(N, x, n, sv, sb);
   double lambda = 1e-7;
-  if (!(sse_t / den > 1e-7 * (1.0 + kCertMargin))) {
-    double run = 0.0;
-    for (int base = 0; base < n; base += 32) {
-      const int i = base + c.lane;
-      fold_exact_chunk(c, i < n ? resid(i) : 0.0, min(32, n - base), run);
-    }
-    const double v = __shfl_sync(NX_FULL, run, 0) / den;
+  if (!((sv - sb) / den > 1e-7 * (1.0 + 8.0 * kU))) {
+    const double v = sse_x_exact(c, S, kB, kS, x) / den;
     lambda = (v < 1e-7) ? v : 1e-7;
   }
   if (lambda > 1e-14) {
     double a[5][5], bb[5];
 #pragma unroll
     for (int i = 0; i < 5; ++i) {
-      bb[i] = atb[i];
+      bb[i] = N.t[i];
 #pragma unroll
-      for (int j = 0; j < 5; ++j) a[i][j] = ata[i][j];
+      for (int j = 0; j < 5; ++j) a[i][j] = N.A[i][j];
     }
 #pragma unroll
     for (int i = 0; i < 5; ++i) {
-      const double d = lambda * ata[i][i];
+      const double d = lambda * N.A[i][i];
       a[i][i] += d;
       bb[i] += d * prior[i];
     }
@@ -471,21 +677,19 @@ __device__ FitOut gauged_fit(Ctx& c, const Window& w, const Params& cur, double 
   p.tauB = x[3] < 0.0 ? 0.0 : x[3];
   p.tauS = x[4] < 0.0 ? 0.0 : x[4];
   out.p = p;
-  // windowed_sse(samples, p) reusing this fit's factors (same kB, kS)
-  part = 0.0;
-  for (int i = c.lane; i < n; i += 32) {
-    const int k = w.slot(i);
-    const int bi = w.rb[k];
-    const double b = bi, s = w.rs[k], y = w.ry[k];
-    const double fb = clamp_factor(bi <= tab ? fbt[bi] : raw_factor(kB, b));
-    const double thr = p.p_max * fb * clamp_factor(fs_cache[i]);
-    const double work = p.w0 + p.ws * s;
-    const double T = p.tau0 + work / thr + p.tauB * b + p.tauS * s;
-    const double r = (y - T) / y;
-    part += r * r;
-  }
-  out.err = warp_sum(part);
+  const double xp[5] = {p.tau0, aa, cc, p.tauB, p.tauS};  // T(p) == xp . row
+  closed_sse(N, xp, n, out.err, out.bound);
   return out;
+}
+
+// Certified "exact(a) < exact(b) * f" for two windowed-SSE intervals; exact
+// re-evaluation only when the intervals cannot decide.
+__device__ bool less_scaled(Ctx& c, const Stage& S, const FitOut& a, const FitOut& b, double f) {
+  const double a_hi = a.err + a.bound, a_lo = a.err - a.bound;
+  const double b_hi = (b.err + b.bound) * f, b_lo = (b.err - b.bound) * f;
+  if (a_hi < b_lo * (1.0 - 4.0 * kU)) return true;
+  if (a_lo > b_hi * (1.0 + 4.0 * kU)) return false;
+  return wsse_exact(c, S, a.p) < wsse_exact(c, S, b.p) * f;
 }
 
 __device__ void update_structural(Ctx& c, int e) {
@@ -494,30 +698,28 @@ __device__ void update_structural(Ctx& c, int e) {
   const int n = w.n;
   if (n < c.d->min_s || n < 5) return;
   const Params cur = g.lp;
-  bool unsat = false;
-  int shaped = 0, bmax = 1;
-  for (int i = c.lane; i < n; i += 32) {
-    const int k = w.slot(i);
-    const int b = w.rb[k], s = w.rs[k];
-    if (cur.kB * static_cast<double>(b) < 20.0 || cur.kS * static_cast<double>(s) < 20.0) unsat = true;
-    if (s >= 64 && s >= 4 * b) ++shaped;
-    bmax = max(bmax, b);
-  }
-  const bool saturated = !__any_sync(NX_FULL, unsat);
-  shaped = static_cast<int>(__reduce_add_sync(NX_FULL, static_cast<unsigned>(shaped)));
-  bmax = warp_max_int(bmax);
+  Stage S = stage_of(c);
+  bool saturated;
+  int shaped, bmax;
+  stage_window(c, w, cur, S, saturated, shaped, bmax);
   if (saturated || shaped < 16) {
     __syncwarp();
     if (c.lane == 0) g.cnt[6] += 1;
     __syncwarp();
     return;
   }
-  const double base_t = wsse_tree(c, w, cur);
+  if (c.lane == 0) c.rs->work[4] += n;
+  // base_err: direct evaluation, tree order; tree vs left fold of n positive
+  // terms differ by at most 2(n-1)u of the sum
+  FitOut base;
+  base.p = cur;
+  base.err = wsse_tree(c, S, cur);
+  base.bound = 2.0 * (static_cast<double>(n) + 2.0) * kU * base.err;
   const double lo = log(1e-8), hi = log(1e4);
   const double shrink = 1.0 - 1e-3;
   double th0 = log(cur.kB), th1 = log(cur.kS);
   double st0 = 0.5, st1 = 0.5;
-  FitOut best = gauged_fit(c, w, cur, exp(th0), exp(th1), bmax);
+  FitOut best = gauged_fit(c, S, cur, exp(th0), exp(th1));
   if (!isfinite(best.err)) {
     __syncwarp();
     if (c.lane == 0) g.cnt[5] += 1;
@@ -527,8 +729,8 @@ __device__ void update_structural(Ctx& c, int e) {
   const double kbs[3] = {0.05, 0.7, 8.0}, kss[3] = {0.002, 0.03, 0.4};
   for (int a = 0; a < 3; ++a) {
     for (int bq = 0; bq < 3; ++bq) {
-      const FitOut cand = gauged_fit(c, w, cur, kbs[a], kss[bq], bmax);
-      if (isfinite(cand.err) && less_scaled(c, w, cand.err, cand.p, best.err, best.p, shrink)) {
+      const FitOut cand = gauged_fit(c, S, cur, kbs[a], kss[bq]);
+      if (isfinite(cand.err) && less_scaled(c, S, cand, best, shrink)) {
         th0 = log(kbs[a]);
         th1 = log(kss[bq]);
         best = cand;
@@ -546,8 +748,8 @@ __device__ void update_structural(Ctx& c, int e) {
         const double v = tc + sgn * (cdim == 0 ? st0 : st1);
         tc = (v < lo) ? lo : ((hi < v) ? hi : v);
         if (tc == (cdim == 0 ? th0 : th1)) continue;
-        const FitOut cand = gauged_fit(c, w, cur, exp(t0), exp(t1), bmax);
-        if (isfinite(cand.err) && less_scaled(c, w, cand.err, cand.p, best.err, best.p, shrink)) {
+        const FitOut cand = gauged_fit(c, S, cur, exp(t0), exp(t1));
+        if (isfinite(cand.err) && less_scaled(c, S, cand, best, shrink)) {
           th0 = t0;
           th1 = t1;
           best = cand;
@@ -563,9 +765,9 @@ __device__ void update_structural(Ctx& c, int e) {
   }
   // reject if invalid or worse than the current model (learner.cpp:432-435)
   bool worse;
-  if (best.err > base_t * (1.0 + kCertMargin)) worse = true;
-  else if (best.err < base_t * (1.0 - kCertMargin)) worse = false;
-  else worse = wsse_exact(c, w, best.p) > wsse_exact(c, w, cur);
+  if (best.err - best.bound > (base.err + base.bound) * (1.0 + 4.0 * kU)) worse = true;
+  else if (best.err + best.bound < (base.err - base.bound) * (1.0 - 4.0 * kU)) worse = false;
+  else worse = wsse_exact(c, S, best.p) > wsse_exact(c, S, cur);
   if (!params_valid(best.p) || worse) {
     __syncwarp();
     if (c.lane == 0) g.cnt[5] += 1;
@@ -607,8 +809,14 @@ __device__ void record_sample(Ctx& c, int e, int b, int s, double y) {
   }
   __syncwarp();
   const int64_t seen = g.seen;
-  if (seen % c.d->l_period == 0) update_linear(c, e);
-  if (seen >= c.d->min_s && seen % c.d->s_period == 0) update_structural(c, e);
+  if (seen % c.d->l_period == 0) {
+    PhaseTimer pt(c.rs, 5);
+    update_linear(c, e);
+  }
+  if (seen >= c.d->min_s && seen % c.d->s_period == 0) {
+    PhaseTimer pt(c.rs, 6);
+    update_structural(c, e);
+  }
 }
 
 }  // namespace nxd

@@ -54,13 +54,43 @@ __device__ __forceinline__ double throughput(const Params& p, double b, double s
 __device__ __forceinline__ int64_t to_us(double ms) { return llround(ms * 1000.0); }
 __device__ __forceinline__ double to_ms(int64_t us) { return static_cast<double>(us) / 1000.0; }
 
-__device__ __forceinline__ uint64_t fnv1a(uint64_t h, uint64_t v) {  // sim.cpp:24-30
+// FNV-1a over the 8 little-endian bytes of v (sim.cpp:24-30).
+__device__ __forceinline__ uint64_t fnv1a(uint64_t h, uint64_t v) {
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     h ^= (v >> (8 * i)) & 0xff;
     h *= 0x100000001b3ULL;
   }
   return h;
+}
+
+// P^k for the FNV prime P: a zero byte leaves h ^ 0 = h, so k trailing zero
+// bytes of a field collapse into one multiply by P^k.
+constexpr uint64_t kFnvP1 = 0x00000100000001b3ull, kFnvP3 = 0x08a97b0004e7feabull,
+                   kFnvP4 = 0x9ffaac085635bc91ull, kFnvP7 = 0xc5527b8a51d3d2dbull;
+
+__device__ __forceinline__ uint64_t fnv_bytes(uint64_t h, uint64_t v, int nbytes) {
+#pragma unroll
+  for (int i = 0; i < nbytes; ++i) {
+    h ^= (v >> (8 * i)) & 0xff;
+    h *= kFnvP1;
+  }
+  return h;
+}
+
+// The event fingerprint of sim.cpp:302-305 — fnv1a over (time_us, kind,
+// engine_id + 1, request_id). Straight-line fast path for the common widths
+// (time < 2^40 us, engine id + 1 < 256, request id < 2^32): 11 byte rounds +
+// 4 power multiplies instead of 32 rounds; identical value.
+__device__ __forceinline__ uint64_t fnv_event(uint64_t h, uint64_t t, uint64_t kind, uint64_t eid1,
+                                              uint64_t rid) {
+  if ((t >> 40) == 0 && (eid1 >> 8) == 0 && (rid >> 32) == 0 && (kind >> 8) == 0) {
+    h = fnv_bytes(h, t, 5) * kFnvP3;
+    h = ((h ^ kind) * kFnvP1) * kFnvP7;
+    h = ((h ^ eid1) * kFnvP1) * kFnvP7;
+    return fnv_bytes(h, rid, 4) * kFnvP4;
+  }
+  return fnv1a(fnv1a(fnv1a(fnv1a(h, t), kind), eid1), rid);
 }
 
 // xoshiro256++ (proj/include/servesim/rng.h:19-45)

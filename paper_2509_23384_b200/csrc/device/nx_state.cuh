@@ -23,21 +23,26 @@ struct EngSm {
   double lat_sum;
   double rep_lhat, rep_wload, rep_mfree, rep_pmax, rep_at;  // router's report copy
   uint64_t rng[4];
+  double noise[32];                            // next oracle noise multipliers exp(sigma z)
   uint64_t step_t, learn_t, report_t;          // pending-event slots (kNoEvent = none)
+  uint64_t dq_t0;                              // head of the delivery FIFO (cached)
   int64_t started_us, seen, rep_qlen, tw_degen;
   int64_t cnt[7];                              // LearnerCounters
-  uint32_t step_seq, learn_seq, report_seq;
+  uint32_t step_seq, learn_seq, report_seq, dq_s0;
   int32_t wq_head, wq_len, rq_len;
   int32_t pinned, reserved, cache_blocks, lru_head, lru_tail;
-  int32_t busy, plan_n, plan_b, plan_s, plan_wspan, plan_overload;
+  int32_t busy, plan_n, plan_b, plan_s, plan_wspan, plan_overload, plan_ndec;
   int32_t learn_b, learn_s;
   int32_t ring_size, ring_head, tw_head, tw_len, dq_head, dq_len, lat_head, lat_len;
-  int32_t has_rep;
+  int32_t has_rep, noise_pos;
 };
 
 struct RepSm {
   uint64_t ev_hash, rr_next, rng[4];
+  uint64_t next_arr;                           // arrival time at the cursor (cached)
   int64_t arrived, rejected, pending, n_rec, events, info;
+  int64_t work[6];
+  int64_t cycles[8];
   double l_bar_ema;
   uint32_t next_seq;
   int32_t cursor, status, site;
@@ -74,5 +79,24 @@ __device__ __forceinline__ void fail(Ctx& c, int status, int site, int64_t info)
   __syncwarp();
 }
 __device__ __forceinline__ bool failed(const Ctx& c) { return c.rs->status != 0; }
+
+__device__ __forceinline__ long long nx_clock() {
+#ifdef __CUDA_ARCH__
+  return clock64();
+#else
+  return 0;
+#endif
+}
+
+// Phase timer: lane 0 charges the SM cycles of a scope to rs->cycles[k].
+struct PhaseTimer {
+  RepSm* rs;
+  int k;
+  long long t0;
+  __device__ __forceinline__ PhaseTimer(RepSm* r, int kk) : rs(r), k(kk), t0(nx_clock()) {}
+  __device__ __forceinline__ ~PhaseTimer() {
+    if (lane_id() == 0) rs->cycles[k] += nx_clock() - t0;
+  }
+};
 
 }  // namespace nxd

@@ -68,10 +68,12 @@ __device__ __forceinline__ int lower_bound_prefix(const int32_t* pre, int hi, in
   return lo;
 }
 
+// Publishes a plan: n allocations whose first `ndec` are run-queue decodes.
 __device__ __forceinline__ void set_plan(Ctx& c, EngSm& g, int n, int b, int s, double pred,
-                                         double target, int wspan, int overload) {
+                                         double target, int wspan, int overload, int ndec) {
   __syncwarp();
   if (c.lane == 0) {
+    g.plan_ndec = ndec;
     g.plan_n = n;
     g.plan_b = b;
     g.plan_s = s;
@@ -105,26 +107,34 @@ __device__ void plan_lens(Ctx& c, int e) {
   const double target = target_latency(c, g, W);
   if (R > qmax) {  // transient overload: truncated decode plan (lens.cpp:108-117)
     write_decodes(c, rq, qmax, preq, ptok);
-    set_plan(c, g, qmax, qmax, qmax, predict(P, qmax, qmax), target, 0, 1);
+    set_plan(c, g, qmax, qmax, qmax, predict(P, qmax, qmax), target, 0, 1, qmax);
     return;
   }
   if (!(target > 0.0)) {  // binary_search_budget precondition (lens.cpp:36-38)
     fail(c, 1, NX_SITE_BISECT, 0);
     return;
   }
+  if (W == 0) {
+    // Empty wait queue: the only candidate is B = R with S = R (avail = R),
+    // so the sweep reduces to one prediction (lens.cpp:121-146).
+    write_decodes(c, rq, R, preq, ptok);
+    set_plan(c, g, R, R, R, predict(P, R, R), target, 0, 0, R);
+    return;
+  }
   const int b_lo = R > 1 ? R : 1;
   const int b_hi = (R + W < qmax) ? R + W : qmax;
   const int span = b_hi - R;
   build_prefix(c, wq, span);
+  if (c.lane == 0) c.rs->work[2] += span;
   const int32_t* pre = c.prefix;
   const double thr_eps = target * c.d->eps_ratio;
   const int iters = c.d->n_iters;
-  double best_err = kInf;
+  double best_err = kInf, best_T = 0.0;
   int best_budget = -1;
   for (int B0 = b_lo; B0 <= b_hi; B0 += 32) {
     const int B = B0 + c.lane;
     const bool act = B <= b_hi;
-    double err = kInf;
+    double err = kInf, T = 0.0;
     int budget = 0;
     if (act) {
       const int avail = R + pre[B - R];
@@ -146,13 +156,15 @@ __device__ void plan_lens(Ctx& c, int e) {
       }
       // realize(allocate_tokens(...)): S = budget, b = R + first j with prefix[j] >= budget - R
       const int j = lower_bound_prefix(pre, B - R, budget - R);
-      err = fabs(predict(P, static_cast<double>(R + j), static_cast<double>(budget)) - target);
+      T = predict(P, static_cast<double>(R + j), static_cast<double>(budget));
+      err = fabs(T - target);
     }
     // first B whose error is below eps*target ends the sweep (the sequential
     // loop's early exit fires exactly there); otherwise keep the first strict min
     const unsigned hit = __ballot_sync(NX_FULL, act && err < thr_eps);
     if (hit) {
       best_budget = __shfl_sync(NX_FULL, budget, __ffs(hit) - 1);
+      best_T = __shfl_sync(NX_FULL, T, __ffs(hit) - 1);
       break;
     }
     double v = (act && !isnan(err)) ? err : kInf;
@@ -166,13 +178,16 @@ __device__ void plan_lens(Ctx& c, int e) {
         who = ow;
       }
     }
+    const int wb = __shfl_sync(NX_FULL, budget, who & 31);
+    const double wT = __shfl_sync(NX_FULL, T, who & 31);
     if (v < best_err) {
       best_err = v;
-      best_budget = __shfl_sync(NX_FULL, budget, who);
+      best_budget = wb;
+      best_T = wT;
     }
   }
   if (best_budget < 0) {  // every candidate error was NaN: empty plan
-    set_plan(c, g, 0, 0, 0, 0.0, target, 0, 0);
+    set_plan(c, g, 0, 0, 0, 0.0, target, 0, 0, 0);
     return;
   }
   const int need = best_budget - R;
@@ -184,8 +199,7 @@ __device__ void plan_lens(Ctx& c, int e) {
     preq[R + k] = wq[k];
     ptok[R + k] = rem < left ? rem : left;
   }
-  set_plan(c, g, R + j, R + j, best_budget,
-           predict(P, static_cast<double>(R + j), static_cast<double>(best_budget)), target, j, 0);
+  set_plan(c, g, R + j, R + j, best_budget, best_T, target, j, 0, R);
 }
 
 // ---- baseline engine policies (engine.cpp:61-108) -------------------------------
@@ -218,10 +232,10 @@ __device__ void plan_baseline(Ctx& c, int e) {
         ptok[k] = c.prefix[k + 1] - c.prefix[k];
       }
       const int s = c.prefix[j];
-      set_plan(c, g, j, j, s, predict(P, j, s), 0.0, j, 0);
+      set_plan(c, g, j, j, s, predict(P, j, s), 0.0, j, 0, 0);
     } else {
       write_decodes(c, rq, R, preq, ptok);
-      set_plan(c, g, R, R, R, predict(P, R, R), 0.0, 0, 0);
+      set_plan(c, g, R, R, R, predict(P, R, R), 0.0, 0, 0, R);
     }
     return;
   }
@@ -250,7 +264,7 @@ __device__ void plan_baseline(Ctx& c, int e) {
   }
   const int stot = R + static_cast<int>(__reduce_add_sync(NX_FULL, static_cast<unsigned>(part)));
   const int n = R + jj;
-  set_plan(c, g, n, n, stot, n > 0 ? predict(P, n, stot) : 0.0, 0.0, jj, 0);
+  set_plan(c, g, n, n, stot, n > 0 ? predict(P, n, stot) : 0.0, 0.0, jj, 0, R);
 }
 
 // ---- trim_for_kv (engine.cpp:184-214) ----------------------------------------------
@@ -259,12 +273,12 @@ __device__ void trim_for_kv(Ctx& c, int e) {
   const NxEngineDesc& ed = c.ed[e];
   int32_t* preq = c.P->plan_req + ed.plan_off;
   int32_t* ptok = c.P->plan_tok + ed.plan_off;
-  const int n = g.plan_n;
+  const int n = g.plan_n, ndec = g.plan_ndec;
   __syncwarp();
   if (c.lane == 0) {
-    int kept = 0;
+    int kept = ndec;  // decodes are always kept (growth already reserved)
     bool trimmed = false;
-    for (int k = 0; k < n; ++k) {
+    for (int k = ndec; k < n; ++k) {
       const int r = preq[k];
       const int tok = ptok[k];
       bool keep;
@@ -292,8 +306,8 @@ __device__ void trim_for_kv(Ctx& c, int e) {
       }
     }
     if (kept != n) {
-      int s = 0;
-      for (int k = 0; k < kept; ++k) s += ptok[k] < 0 ? 1 : ptok[k];
+      int s = ndec;
+      for (int k = ndec; k < kept; ++k) s += ptok[k];
       g.plan_n = kept;
       g.plan_b = kept;
       g.plan_s = s;
@@ -303,33 +317,54 @@ __device__ void trim_for_kv(Ctx& c, int e) {
   __syncwarp();
 }
 
+// Oracle noise (engine.cpp:128-132): the engine stream draws two uniforms per
+// executed step; 32 steps' worth are drawn at once (lane 0, in stream order)
+// and the Box-Muller + exp for each step runs on its own lane.
+__device__ void refill_noise(Ctx& c, int e) {
+  EngSm& g = c.eng[e];
+  __syncwarp();
+  if (c.lane == 0) {
+    Rng rng;
+    for (int i = 0; i < 4; ++i) rng.s[i] = g.rng[i];
+    for (int k = 0; k < 64; ++k) c.chunk[k] = rng.uniform();
+    for (int i = 0; i < 4; ++i) g.rng[i] = rng.s[i];
+  }
+  __syncwarp();
+  const double u1 = c.chunk[2 * c.lane], u2 = c.chunk[2 * c.lane + 1];
+  const double z = sqrt(-2.0 * log(u1)) * cos((2.0 * 3.141592653589793) * u2);
+  g.noise[c.lane] = exp(c.ed[e].noise_sigma * z);
+  __syncwarp();
+  if (c.lane == 0) g.noise_pos = 0;
+  __syncwarp();
+}
+
 // ---- begin_step (engine.cpp:216-228) + step event (sim.cpp:143-166) ----------------
 __device__ void try_begin_step(Ctx& c, int e, int64_t now_us) {
   EngSm& g = c.eng[e];
   __syncwarp();
   if (g.busy || (g.wq_len == 0 && g.rq_len == 0)) return;
+  PhaseTimer pt(c.rs, 2);
   const NxEngineDesc& ed = c.ed[e];
   if (ed.policy == 0) plan_lens(c, e);
   else plan_baseline(c, e);
   if (failed(c) || g.plan_n == 0) return;
   trim_for_kv(c, e);
   if (g.plan_n == 0) return;
+  const bool noisy = ed.noise_sigma != 0.0;
+  if (noisy && g.noise_pos >= 32) refill_noise(c, e);
   __syncwarp();
   if (c.lane == 0) {
     const Params tp = params_from(ed.tp);
     double actual = predict(tp, g.plan_b, g.plan_s);  // oracle_latency (engine.cpp:128-132)
-    if (ed.noise_sigma != 0.0) {
-      Rng rng;
-      for (int i = 0; i < 4; ++i) rng.s[i] = g.rng[i];
-      actual = actual * exp(ed.noise_sigma * rng.normal());
-      for (int i = 0; i < 4; ++i) g.rng[i] = rng.s[i];
-    }
+    if (noisy) actual = actual * g.noise[g.noise_pos++];
     const int64_t d = to_us(actual);
     g.busy = 1;
     g.started_us = now_us;
     g.actual = actual;
     g.step_t = static_cast<uint64_t>(now_us + (d > 1 ? d : 1));
     g.step_seq = c.rs->next_seq++;
+    c.rs->work[0] += 1;
+    c.rs->work[1] += g.plan_b;
   }
   __syncwarp();
 }
@@ -461,6 +496,7 @@ __device__ void step_complete(Ctx& c, int e, int64_t now_us) {
   int* st_req = st_sess + 96;
   int pinned = g.pinned;
   int dsum = 0, n_fin = 0, n_first = 0;
+  const long long t_cs = nx_clock();
   put(g.busy, 0);
   for (int base = 0; base < n; base += 32) {
     const int k = base + c.lane;
@@ -618,6 +654,7 @@ __device__ void step_complete(Ctx& c, int e, int64_t now_us) {
   }
   __syncwarp();
   if (n_fin) tradeoff_refit(c, e);
+  if (c.lane == 0) c.rs->cycles[3] += nx_clock() - t_cs;
   try_begin_step(c, e, now_us);
 }
 
@@ -651,8 +688,10 @@ __device__ void state_report(Ctx& c, int e, int64_t now_us) {
     } else {
       const int slot = (g.dq_head + g.dq_len) % ed.dq_cap;
       const int64_t o = ed.dq_off + slot;
-      c.P->dq_t[o] = now_us + ed.stale_us;
-      c.P->dq_seq[o] = c.rs->next_seq++;
+      const int64_t dt = now_us + ed.stale_us;
+      const uint32_t ds = c.rs->next_seq++;
+      c.P->dq_t[o] = dt;
+      c.P->dq_seq[o] = ds;
       double* sv = c.P->dq_sv + 5 * o;
       sv[0] = l_hat;
       sv[1] = w_load;
@@ -660,6 +699,10 @@ __device__ void state_report(Ctx& c, int e, int64_t now_us) {
       sv[3] = g.lp.p_max;
       sv[4] = now;
       c.P->dq_qlen[o] = q;
+      if (g.dq_len == 0) {
+        g.dq_t0 = static_cast<uint64_t>(dt);
+        g.dq_s0 = ds;
+      }
       g.dq_len += 1;
     }
     g.report_t = static_cast<uint64_t>(now_us + ed.period_us);
@@ -889,10 +932,11 @@ __device__ void init_replica(Ctx& c) {
     for (int i = 0; i < 7; ++i) g.cnt[i] = 0;
     g.wq_head = 0; g.wq_len = 0; g.rq_len = 0;
     g.pinned = 0; g.reserved = 0; g.cache_blocks = 0; g.lru_head = -1; g.lru_tail = -1;
-    g.busy = 0; g.plan_n = 0; g.plan_b = 0; g.plan_s = 0; g.plan_wspan = 0; g.plan_overload = 0;
+    g.busy = 0; g.plan_n = 0; g.plan_b = 0; g.plan_s = 0; g.plan_wspan = 0; g.plan_overload = 0; g.plan_ndec = 0;
     g.learn_b = 0; g.learn_s = 0;
     g.ring_size = 0; g.ring_head = 0; g.tw_head = 0; g.tw_len = 0;
     g.dq_head = 0; g.dq_len = 0; g.lat_head = 0; g.lat_len = 0; g.has_rep = 0;
+    g.dq_t0 = kNoEvent; g.dq_s0 = 0; g.noise_pos = 32;
   }
   if (c.lane == 0) {
     RepSm& R = *c.rs;
@@ -900,9 +944,12 @@ __device__ void init_replica(Ctx& c) {
     R.rr_next = 0;
     for (int i = 0; i < 4; ++i) R.rng[i] = d.router_rng[i];
     R.arrived = 0; R.rejected = 0; R.pending = c.n_req; R.n_rec = 0; R.events = 0; R.info = 0;
+    for (int i = 0; i < 6; ++i) R.work[i] = 0;
+    for (int i = 0; i < 8; ++i) R.cycles[i] = 0;
     R.l_bar_ema = 128.0;
     R.next_seq = static_cast<uint32_t>(c.n_eng + c.n_req);  // arrival i carries seq E + i
     R.cursor = 0; R.status = 0; R.site = 0;
+    R.next_arr = c.n_req > 0 ? static_cast<uint64_t>(c.P->arr_us[c.roff]) : kNoEvent;
   }
   __syncwarp();
 }
@@ -912,6 +959,7 @@ __device__ void run_replica(Ctx& c) {
   const NxReplicaDesc& d = *c.d;
   const uint64_t duration = static_cast<uint64_t>(d.duration_us);
   while (!failed(c)) {
+    long long t_sel = nx_clock();
     // ---- next event: warp-wide (time, seq) minimum over the slots ----
     uint64_t t = kNoEvent;
     uint32_t sq = 0xffffffffu;
@@ -925,15 +973,12 @@ __device__ void run_replica(Ctx& c) {
       if (g.learn_t < t || (g.learn_t == t && g.learn_t != kNoEvent && g.learn_seq < sq)) {
         t = g.learn_t; sq = g.learn_seq; kind = 3;
       }
-      if (g.dq_len > 0) {
-        const int64_t o = c.ed[c.lane].dq_off + g.dq_head;
-        const uint64_t dt = static_cast<uint64_t>(c.P->dq_t[o]);
-        const uint32_t ds = c.P->dq_seq[o];
-        if (dt < t || (dt == t && ds < sq)) { t = dt; sq = ds; kind = 4; }
+      if (g.dq_t0 < t || (g.dq_t0 == t && g.dq_t0 != kNoEvent && g.dq_s0 < sq)) {
+        t = g.dq_t0; sq = g.dq_s0; kind = 4;
       }
     }
-    if (c.lane == 0 && c.rs->cursor < c.n_req) {
-      const uint64_t at = static_cast<uint64_t>(c.P->arr_us[c.roff + c.rs->cursor]);
+    if (c.lane == 0 && c.rs->next_arr != kNoEvent) {
+      const uint64_t at = c.rs->next_arr;
       const uint32_t as = static_cast<uint32_t>(c.n_eng + c.rs->cursor);
       if (at < t || (at == t && as < sq)) { t = at; sq = as; kind = 0; }
     }
@@ -962,13 +1007,24 @@ __device__ void run_replica(Ctx& c) {
     __syncwarp();
     if (c.lane == 0) {
       EngSm& g = c.eng[kind == 0 ? 0 : who];
-      if (kind == 0) c.rs->cursor += 1;
+      if (kind == 0) {
+        const int nc = c.rs->cursor + 1;
+        c.rs->cursor = nc;
+        c.rs->next_arr = nc < c.n_req ? static_cast<uint64_t>(c.P->arr_us[c.roff + nc]) : kNoEvent;
+      }
       else if (kind == 1) g.step_t = kNoEvent;
       else if (kind == 2) g.report_t = kNoEvent;
       else if (kind == 3) g.learn_t = kNoEvent;
       else {
         g.dq_head = (g.dq_head + 1) % c.ed[who].dq_cap;
         g.dq_len -= 1;
+        if (g.dq_len > 0) {
+          const int64_t o = c.ed[who].dq_off + g.dq_head;
+          g.dq_t0 = static_cast<uint64_t>(c.P->dq_t[o]);
+          g.dq_s0 = c.P->dq_seq[o];
+        } else {
+          g.dq_t0 = kNoEvent;
+        }
       }
     }
     __syncwarp();
@@ -976,13 +1032,12 @@ __device__ void run_replica(Ctx& c) {
     if (kind == 2 && c.rs->pending == 0 && c.rs->arrived - c.rs->rejected - c.rs->n_rec == 0) continue;
     __syncwarp();
     if (c.lane == 0) {
-      uint64_t h = c.rs->ev_hash;
-      h = fnv1a(h, now_u);
-      h = fnv1a(h, static_cast<uint64_t>(kind));
-      h = fnv1a(h, kind == 0 ? 0ull : static_cast<uint64_t>(c.ed[who].engine_id + 1));
-      h = fnv1a(h, static_cast<uint64_t>(rid));
+      const uint64_t h = fnv_event(c.rs->ev_hash, now_u, static_cast<uint64_t>(kind),
+                                   kind == 0 ? 0ull : static_cast<uint64_t>(c.ed[who].engine_id + 1),
+                                   static_cast<uint64_t>(rid));
       c.rs->ev_hash = h;
       c.rs->events += 1;
+      c.rs->cycles[0] += nx_clock() - t_sel;
     }
     __syncwarp();
     switch (kind) {
@@ -993,13 +1048,16 @@ __device__ void run_replica(Ctx& c) {
           c.rs->pending -= 1;
         }
         __syncwarp();
-        const int e = route(c, rid, to_ms(now));
-        if (failed(c)) break;
-        int ok = 0;
-        if (c.lane == 0) {
-          ok = admit(c, e, rid) ? 1 : 0;
-          if (!ok) c.rs->rejected += 1;
+        int e, ok = 0;
+        {
+          PhaseTimer pt(c.rs, 1);
+          e = route(c, rid, to_ms(now));
+          if (c.lane == 0 && !failed(c)) {
+            ok = admit(c, e, rid) ? 1 : 0;
+            if (!ok) c.rs->rejected += 1;
+          }
         }
+        if (failed(c)) break;
         ok = __shfl_sync(NX_FULL, ok, 0);
         __syncwarp();
         if (ok) try_begin_step(c, e, now);
@@ -1008,15 +1066,18 @@ __device__ void run_replica(Ctx& c) {
       case 1:
         step_complete(c, who, now);
         break;
-      case 2:
+      case 2: {
+        PhaseTimer pt(c.rs, 4);
         state_report(c, who, now);
         break;
+      }
       case 3: {
         const EngSm& g = c.eng[who];
         record_sample(c, who, g.learn_b, g.learn_s, g.learn_y);
         break;
       }
       case 4: {  // report delivery -> Router::on_report (router.cpp:75-81)
+        PhaseTimer pt(c.rs, 7);
         __syncwarp();
         if (c.lane == 0) {
           EngSm& g = c.eng[who];
@@ -1049,6 +1110,8 @@ __device__ void write_outputs(Ctx& c, int r) {
     o.status = R.status;
     o.err_site = R.site;
     o.err_info = R.info;
+    for (int i = 0; i < 6; ++i) o.work[i] = R.work[i];
+    for (int i = 0; i < 8; ++i) o.cycles[i] = R.cycles[i];
   }
   for (int e = c.lane; e < c.n_eng; e += 32) {
     const EngSm& g = c.eng[e];

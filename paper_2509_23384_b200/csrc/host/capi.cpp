@@ -196,7 +196,7 @@ void fill_descriptors(nx_sim& h) {
     d.min_s = static_cast<int32_t>(std::min<int64_t>(c.min_structural, INT32_MAX));
     req_off += n;
     sess_off += ns;
-    scratch_off += static_cast<int64_t>(c.long_window) + 1024 + 2 * c.short_window + 64;
+    scratch_off += (9 * static_cast<int64_t>(c.long_window) + 1024 + 10240 + 64 + 31) / 32 * 32;  // nx_learner.cuh layout
     for (const auto& ec : c.engines) {
       NxEngineDesc e;
       std::memset(&e, 0, sizeof e);
@@ -635,6 +635,29 @@ int nx_sim_learner(nx_sim_t h, int32_t replica, int32_t engine, double* params8,
     for (int i = 0; i < 8; ++i) params8[i] = eo.params[i];
     *samples = eo.samples;
     for (int i = 0; i < 7; ++i) counters7[i] = eo.counters[i];
+  });
+}
+
+int nx_sim_work(nx_sim_t h, int32_t replica, int64_t* out6) {
+  return guard([&] {
+    if (replica < 0 || replica >= h->n_rep) throw std::invalid_argument("replica out of range");
+    for (int i = 0; i < 6; ++i) out6[i] = h->h_rep_out[replica].work[i];
+  });
+}
+
+int nx_sim_phase_cycles(nx_sim_t h, int32_t replica, int64_t* out8) {
+  return guard([&] {
+    if (replica < 0 || replica >= h->n_rep) throw std::invalid_argument("replica out of range");
+    for (int i = 0; i < 8; ++i) out8[i] = h->h_rep_out[replica].cycles[i];
+  });
+}
+
+int nx_sim_copy_summaries(nx_sim_t h, void* dst_dev) {
+  return guard([&] {
+    cuda_check(cudaMemcpyAsync(dst_dev, h->pools.rep_out,
+                               static_cast<size_t>(h->n_rep) * sizeof(NxReplicaOut),
+                               cudaMemcpyDeviceToDevice, h->stream), "D2D summaries");
+    cuda_check(cudaStreamSynchronize(h->stream), "sync");
   });
 }
 

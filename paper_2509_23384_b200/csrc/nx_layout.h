@@ -54,6 +54,16 @@ typedef struct NxReplicaOut {
   int32_t status;          /* 0 ok, 1 invalid_argument, 2 runtime_error, 3 logic_error */
   int32_t err_site;        /* NX_SITE_* where the error was raised */
   int64_t err_info;
+  /* work counters for the roofline's algorithmic bytes:
+     [0] executed steps, [1] sum of step batch sizes b, [2] sum of LENS
+     candidate windows (waiters scanned), [3] linear-refit window samples,
+     [4] structural-refit window samples (fits run), [5] gauged fits */
+  int64_t work[6];
+  /* SM cycles spent per phase (clock64, lane 0): [0] event selection + hash,
+     [1] routing + admission, [2] step planning (LENS / baseline, KV trim,
+     oracle), [3] step completion, [4] state reports, [5] linear refits,
+     [6] structural refits, [7] report deliveries */
+  int64_t cycles[8];
 } NxReplicaOut;
 
 typedef struct NxEngineOut {

@@ -99,6 +99,24 @@ class Batch:
         check(lib().nx_sim_records(self.h, r, arr, n.value, C.byref(n)))
         return list(arr)[: n.value]
 
+    def work(self, r: int):
+        out = (C.c_int64 * 6)()
+        check(lib().nx_sim_work(self.h, r, out))
+        return list(out)
+
+    def phase_cycles(self, r: int):
+        out = (C.c_int64 * 8)()
+        check(lib().nx_sim_phase_cycles(self.h, r, out))
+        return list(out)
+
+    def summaries_nbytes(self) -> int:
+        ptr, n = C.c_void_p(), C.c_int64()
+        check(lib().nx_sim_summaries_dev(self.h, C.byref(ptr), C.byref(n)))
+        return n.value
+
+    def copy_summaries(self, dst_ptr: int):
+        check(lib().nx_sim_copy_summaries(self.h, C.c_void_p(dst_ptr)))
+
     def learner(self, r: int, e: int):
         p = (C.c_double * 8)()
         s = C.c_int64()

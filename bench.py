@@ -161,17 +161,20 @@ def k1_model_eval(torch, dev) -> dict:
     out = torch.empty(n, device=dev, dtype=torch.float64)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
     times = []
     for it in range(8):
         flush.fill_(it & 0xff)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        perf_model.eval_device(params, idx, b, s, out, None, stream=stream)
+        perf_model.eval_device_async(params, idx, b, s, out, status, stream=stream)
         e1.record(stream)
         torch.cuda.synchronize(dev)
         if it >= 3:
             times.append(e0.elapsed_time(e1) / 1e3)
     t = statistics.mean(times)
+    if int(status.item()) != 0:
+        raise RuntimeError("K1 flagged invalid records")
     byts = n * (4 + 4 + 4 + 8)
     pk, src = peaks()
     return {"kernel": "perf_eval_kernel (K1, fp64 deterministic)", "records": n,

@@ -46,6 +46,11 @@ int nx_device_count(void);
 int nx_perf_eval_dev(const double* params, int32_t n_params, const int32_t* idx,
                      const int32_t* b, const int32_t* s, double* out_T, double* out_thr,
                      int64_t n, int32_t mode, void* stream);
+/* Stream-ordered variant: no host synchronisation; bit 0 of *dev_status (a
+ * device word the caller zeroes) is set if any record or row is invalid. */
+int nx_perf_eval_async(const double* params, int32_t n_params, const int32_t* idx,
+                       const int32_t* b, const int32_t* s, double* out_T, double* out_thr,
+                       int64_t n, int32_t mode, uint32_t* dev_status, void* stream);
 int nx_perf_eval_host(const double* params, int32_t n_params, const int32_t* idx,
                       const int32_t* b, const int32_t* s, double* out_T, double* out_thr,
                       int64_t n, int32_t mode);
@@ -121,6 +126,11 @@ int nx_sim_copy_summaries(nx_sim_t h, void* dst_dev);
 /* ---- host utilities (reference workload generator semantics) -------------
  * synth_generate (proj/src/workload.cpp:137-166): prompts/outputs/session
  * ids for n requests. session_ids: n * 16-byte NUL-terminated strings. */
+/* Parse a RunConfig JSON and synthesise its workload on the host only:
+ * arrival fingerprint (sim.cpp:132-139), request and session counts. Raises
+ * the reference's config errors (RunConfig::validate, sim.cpp:418-452). */
+int nx_workload_info(const char* config_json, uint64_t* arrival_hash, int64_t* n_requests,
+                     int64_t* n_sessions);
 int nx_synth_generate(const char* scenario, int64_t n, uint64_t seed, int64_t* prompts,
                       int64_t* outputs, char* session_ids16);
 

@@ -70,8 +70,12 @@ def lib() -> C.CDLL:
     L.nx_sim_summaries_dev.argtypes = [C.c_void_p, _P(C.c_void_p), _P(C.c_int64)]
     L.nx_perf_eval_dev.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
                                    C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p]
+    L.nx_perf_eval_async.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
+                                     C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p,
+                                     C.c_void_p]
     L.nx_perf_eval_host.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
                                     C.c_void_p, C.c_void_p, C.c_int64, C.c_int32]
+    L.nx_workload_info.argtypes = [C.c_char_p, _P(C.c_uint64), _P(C.c_int64), _P(C.c_int64)]
     L.nx_synth_generate.argtypes = [C.c_char_p, C.c_int64, C.c_uint64, _P(C.c_int64),
                                     _P(C.c_int64), C.c_char_p]
     _lib = L

@@ -670,9 +670,9 @@ int nx_sim_summaries_dev(nx_sim_t h, void** dev_ptr, int64_t* bytes) {
 void nx_sim_destroy(nx_sim_t h) { delete h; }
 
 // ---- K1 --------------------------------------------------------------------------
-int nx_perf_eval_dev(const double* params, int32_t n_params, const int32_t* idx, const int32_t* b,
-                     const int32_t* s, double* out_T, double* out_thr, int64_t n, int32_t mode,
-                     void* stream) {
+int nx_perf_eval_async(const double* params, int32_t n_params, const int32_t* idx, const int32_t* b,
+                       const int32_t* s, double* out_T, double* out_thr, int64_t n, int32_t mode,
+                       uint32_t* dev_status, void* stream) {
   return guard([&] {
     if (n < 0 || n_params < 1) throw std::invalid_argument("nx_perf_eval: empty parameter table");
     for (const void* p : {(const void*)idx, (const void*)b, (const void*)s, (const void*)out_T})
@@ -682,13 +682,23 @@ int nx_perf_eval_dev(const double* params, int32_t n_params, const int32_t* idx,
     if (n == 0) return;
     int dev = 0;
     cudaGetDevice(&dev);
+    cuda_check(nx_launch_perf_eval(params, n_params, idx, b, s, out_T, out_thr, n,
+                                   mode == NX_FAST_FP32, dev_status, sm_count(dev),
+                                   static_cast<cudaStream_t>(stream)),
+               "perf_eval launch");
+  });
+}
+
+int nx_perf_eval_dev(const double* params, int32_t n_params, const int32_t* idx, const int32_t* b,
+                     const int32_t* s, double* out_T, double* out_thr, int64_t n, int32_t mode,
+                     void* stream) {
+  return guard([&] {
     static thread_local unsigned* flag = nullptr;
     if (!flag) cuda_check(cudaMalloc(&flag, sizeof(unsigned)), "cudaMalloc(flag)");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     cuda_check(cudaMemsetAsync(flag, 0, sizeof(unsigned), st), "memset");
-    cuda_check(nx_launch_perf_eval(params, n_params, idx, b, s, out_T, out_thr, n,
-                                   mode == NX_FAST_FP32, flag, sm_count(dev), st),
-               "perf_eval launch");
+    const int rc = nx_perf_eval_async(params, n_params, idx, b, s, out_T, out_thr, n, mode, flag, stream);
+    if (rc) throw NxError(rc, g_err);
     unsigned bad = 0;
     cuda_check(cudaMemcpyAsync(&bad, flag, sizeof bad, cudaMemcpyDeviceToHost, st), "D2H flag");
     cuda_check(cudaStreamSynchronize(st), "perf_eval sync");
@@ -722,6 +732,17 @@ int nx_perf_eval_host(const double* params, int32_t n_params, const int32_t* idx
 }
 
 // ---- host utilities -------------------------------------------------------------
+int nx_workload_info(const char* config_json, uint64_t* arrival_hash, int64_t* n_requests,
+                     int64_t* n_sessions) {
+  return guard([&] {
+    const nx::RunCfg c = nx::parse_run_config(config_json);
+    const nx::Workload w = nx::build_workload(c);
+    *arrival_hash = w.arrival_hash;
+    *n_requests = static_cast<int64_t>(w.prompt.size());
+    *n_sessions = static_cast<int64_t>(w.session_names.size());
+  });
+}
+
 int nx_synth_generate(const char* scenario, int64_t n, uint64_t seed, int64_t* prompts,
                       int64_t* outputs, char* session_ids16) {
   return guard([&] {

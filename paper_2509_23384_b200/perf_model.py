@@ -73,6 +73,17 @@ def eval_device(params, idx, b, s, out_T, out_thr=None, mode: int = NX_DETERMINI
                                  idx.numel(), mode, C.c_void_p(sh)))
 
 
+def eval_device_async(params, idx, b, s, out_T, status, out_thr=None,
+                      mode: int = NX_DETERMINISTIC_FP64, stream=None):
+    """Stream-ordered K1 without host sync; `status` is an int32 CUDA tensor
+    of one element the caller zeroes (nonzero afterwards = invalid input)."""
+    sh = stream.cuda_stream if stream is not None else 0
+    check(lib().nx_perf_eval_async(params.data_ptr(), params.shape[0], idx.data_ptr(),
+                                   b.data_ptr(), s.data_ptr(), out_T.data_ptr(),
+                                   out_thr.data_ptr() if out_thr is not None else None,
+                                   idx.numel(), mode, status.data_ptr(), C.c_void_p(sh)))
+
+
 def throughput(params, shape) -> float:
     """servesim::throughput(params, {b, s})."""
     b, s = shape

@@ -203,6 +203,14 @@ def sweep(base: dict, axis: str, values, device: int = 0):
     return {"axis": axis, "rows": rows}
 
 
+def workload_info(cfg):
+    """Host-only: (arrival_hash, n_requests, n_sessions) of a RunConfig."""
+    h, n, ns = C.c_uint64(), C.c_int64(), C.c_int64()
+    text = cfg if isinstance(cfg, str) else json.dumps(cfg)
+    check(lib().nx_workload_info(text.encode(), C.byref(h), C.byref(n), C.byref(ns)))
+    return h.value, n.value, ns.value
+
+
 def synth_generate(scenario: str, n: int, seed: int):
     """workload.cpp:137-166 semantics -> (prompts, outputs, session_ids)."""
     P = (C.c_int64 * n)()

@@ -107,8 +107,10 @@ int nx_sim_records(nx_sim_t h, int32_t replica, nx_request_record* out, int64_t 
 int nx_sim_work(nx_sim_t h, int32_t replica, int64_t* out6);
 /* SM cycles per phase of a replica (lane-0 clock64): [0] event selection +
  * hash, [1] routing + admission, [2] step planning, [3] step completion,
- * [4] state reports, [5] linear refits, [6] structural refits, [7] deliveries */
-int nx_sim_phase_cycles(nx_sim_t h, int32_t replica, int64_t* out8);
+ * [4] state reports, [5] linear refits, [6] structural refits (on the refit
+ * warp, overlapped with the event loop), [7] deliveries, [8] event loop
+ * blocked on a pending refit, [9]-[15] refit internals (diagnostic) */
+int nx_sim_phase_cycles(nx_sim_t h, int32_t replica, int64_t* out10);
 /* Learner state per engine: params[8] + samples + counters[7]. */
 int nx_sim_learner(nx_sim_t h, int32_t replica, int32_t engine, double* params8,
                    int64_t* samples, int64_t* counters7);

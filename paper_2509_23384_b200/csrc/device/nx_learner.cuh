@@ -16,70 +16,88 @@
 namespace nxd {
 
 
-// ---- 5x5 elimination (learner.cpp:24-60), fully unrolled in registers -----
+// ---- 5x5 elimination (learner.cpp:24-60) -------------------------------------
 __device__ __forceinline__ double dmax(double m, double v) { return (m < v) ? v : m; }
 
-__device__ bool solve5(double a[5][5], double b[5], double x[5]) {
-  double scale[5];
+// Warp-parallel form of solve5: lane 5i+j (< 25) holds a[i][j], lane 25+i holds
+// b[i]. Every element sees exactly the serial algorithm's operations in the
+// same order (scaling, pivot choice, row swap, elimination, back
+// substitution), so the result is bitwise identical — without the serial
+// version's 5x5 register arrays (which spilled) or its dependent loops.
+__device__ __forceinline__ double pick5(const double v[5], int k) {
+  double r = v[0];
 #pragma unroll
-  for (int j = 0; j < 5; ++j) {
-    double m = 0.0;
+  for (int q = 1; q < 5; ++q)
+    if (k == q) r = v[q];
+  return r;
+}
+
+__device__ bool solve5_warp(double v, double x[5]) {
+  const int lane = lane_id();
+  const bool isA = lane < 25;
+  const int i = isA ? lane / 5 : (lane < 30 ? lane - 25 : 0);
+  const int j = isA ? lane % 5 : 5;
+  // column scaling (max is exact in any order)
+  double m = 0.0;
 #pragma unroll
-    for (int i = 0; i < 5; ++i) m = dmax(m, fabs(a[i][j]));
-    if (m <= 0.0) return false;
-    scale[j] = 1.0 / m;
+  for (int r = 0; r < 5; ++r) m = dmax(m, fabs(__shfl_sync(NX_FULL, v, r * 5 + (j < 5 ? j : 0))));
+  const bool zero_col = __any_sync(NX_FULL, isA && i == 0 && m <= 0.0);
+  if (zero_col) return false;
+  const double scale = isA ? 1.0 / m : 1.0;
+  if (isA) v *= scale;
+  double sc[5];
 #pragma unroll
-    for (int i = 0; i < 5; ++i) a[i][j] *= scale[j];
-  }
-  double norm = 0.0;
+  for (int q = 0; q < 5; ++q) sc[q] = __shfl_sync(NX_FULL, scale, q);
+  double norm = isA ? fabs(v) : 0.0;
 #pragma unroll
-  for (int i = 0; i < 5; ++i)
-#pragma unroll
-    for (int j = 0; j < 5; ++j) norm = dmax(norm, fabs(a[i][j]));
+  for (int o = 16; o > 0; o >>= 1) norm = dmax(norm, __shfl_xor_sync(NX_FULL, norm, o));
 #pragma unroll
   for (int col = 0; col < 5; ++col) {
+    double cv[5];
+#pragma unroll
+    for (int r = 0; r < 5; ++r) cv[r] = fabs(__shfl_sync(NX_FULL, v, r * 5 + col));
     int piv = col;
-    double pv = fabs(a[col][col]);
+    double pv = cv[col];
 #pragma unroll
-    for (int r = col + 1; r < 5; ++r) {
-      const double v = fabs(a[r][col]);
-      if (v > pv) {
+    for (int r = col + 1; r < 5; ++r)
+      if (cv[r] > pv) {
         piv = r;
-        pv = v;
+        pv = cv[r];
       }
-    }
     if (pv < 1e-10 * norm) return false;
-#pragma unroll
-    for (int r = col + 1; r < 5; ++r) {
-      if (piv == r) {
-#pragma unroll
-        for (int cc = 0; cc < 5; ++cc) {
-          const double t = a[col][cc];
-          a[col][cc] = a[r][cc];
-          a[r][cc] = t;
-        }
-        const double t = b[col];
-        b[col] = b[r];
-        b[r] = t;
-      }
+    // swap rows col <-> piv (A and b lanes alike)
+    int src = lane;
+    if (lane < 30) {
+      const int base = isA ? 0 : 25, stride = isA ? 5 : 1, off = isA ? j : 0;
+      if (i == col) src = base + piv * stride + off;
+      else if (i == piv) src = base + col * stride + off;
     }
-#pragma unroll
-    for (int r = col + 1; r < 5; ++r) {
-      const double f = a[r][col] / a[col][col];
-#pragma unroll
-      for (int cc = col; cc < 5; ++cc) a[r][cc] -= f * a[col][cc];
-      b[r] -= f * b[col];
+    v = __shfl_sync(NX_FULL, v, src);
+    const double diag = __shfl_sync(NX_FULL, v, col * 5 + col);
+    const double pivrow = __shfl_sync(NX_FULL, v, isA ? col * 5 + j : 25 + col);
+    const double arc = __shfl_sync(NX_FULL, v, i * 5 + col);
+    if (lane < 30 && i > col && (j >= col)) {
+      const double f = arc / diag;
+      v -= f * pivrow;
     }
+  }
+  // back substitution (serial order), then undo the column scaling
+  double u[5][5], bb[5];
+#pragma unroll
+  for (int r = 0; r < 5; ++r) {
+#pragma unroll
+    for (int q = r; q < 5; ++q) u[r][q] = __shfl_sync(NX_FULL, v, r * 5 + q);
+    bb[r] = __shfl_sync(NX_FULL, v, 25 + r);
   }
 #pragma unroll
   for (int r = 4; r >= 0; --r) {
-    double acc = b[r];
+    double acc = bb[r];
 #pragma unroll
-    for (int cc = r + 1; cc < 5; ++cc) acc -= a[r][cc] * x[cc];
-    x[r] = acc / a[r][r];
+    for (int q = r + 1; q < 5; ++q) acc -= u[r][q] * x[q];
+    x[r] = acc / u[r][r];
   }
 #pragma unroll
-  for (int j = 0; j < 5; ++j) x[j] *= scale[j];
+  for (int q = 0; q < 5; ++q) x[q] *= sc[q];
   return true;
 }
 
@@ -113,13 +131,34 @@ __device__ __forceinline__ void fold_chunk(const Ctx& c, int cnt, double& acc) {
   }
 }
 
-__device__ __forceinline__ void gather_normal(double acc, double ata[5][5], double atb[5]) {
+
+// Lane element of the normal equations from the 15 unique A^T A entries
+// (slot_of order) and the 5 A^T b entries.
+__device__ __forceinline__ double normal_elem(const double u15[15], const double t5[5]) {
+  const int lane = lane_id();
+  double e = 0.0;
+  if (lane < 25) {
+    const int k = slot_of(lane / 5, lane % 5);
 #pragma unroll
-  for (int i = 0; i < 5; ++i) {
+    for (int q = 0; q < 15; ++q)
+      if (k == q) e = u15[q];
+  } else if (lane < 30) {
 #pragma unroll
-    for (int j = 0; j < 5; ++j) ata[i][j] = __shfl_sync(NX_FULL, acc, slot_of(i, j));
-    atb[i] = __shfl_sync(NX_FULL, acc, 15 + i);
+    for (int q = 0; q < 5; ++q)
+      if (lane - 25 == q) e = t5[q];
   }
+  return e;
+}
+
+// Ridge anchored at `prior` (learner.cpp:86-93): a[i][i] += lambda a[i][i],
+// b[i] += (lambda a[i][i]) prior[i].
+__device__ __forceinline__ double ridge_elem(double e, double lambda, const double prior[5]) {
+  const int lane = lane_id();
+  const int src = (lane >= 25 && lane < 30) ? (lane - 25) * 6 : lane;
+  const double diag = __shfl_sync(NX_FULL, e, src);
+  if (lane < 25 && lane % 6 == 0) return e + lambda * e;
+  if (lane >= 25 && lane < 30) return e + (lambda * diag) * pick5(prior, lane - 25);
+  return e;
 }
 
 // Exact left fold of per-lane values v (valid where `on`) in index order,
@@ -164,8 +203,8 @@ __device__ bool update_linear(Ctx& c, int e) {
   const int n = w.n;
   if (n < 5) return false;
   const Params cur = g.lp;
-  if (c.lane == 0) c.rs->work[3] += n;
-  double* rows = c.scratch + 6 * c.d->long_w + kFbTable;  // (1/thr, s/thr) per sample
+  if (c.lane == 0) count(c.rs->work[3], n);
+  double* rows = c.lin_rows;  // (1/thr, s/thr) per sample; one buffer per warp
   double acc = 0.0;
   for (int base = 0; base < n; base += 32) {
     const int i = base + c.lane;
@@ -188,22 +227,13 @@ __device__ bool update_linear(Ctx& c, int e) {
     __syncwarp();
     fold_chunk(c, min(32, n - base), acc);
   }
-  double ata[5][5], atb[5];
-  gather_normal(acc, ata, atb);
+  // lane element: A^T A slot (lanes < 25) or A^T b (lanes 25..29) from the fold lanes
+  const int src = c.lane < 25 ? slot_of(c.lane / 5, c.lane % 5) : (c.lane < 30 ? 15 + c.lane - 25 : 0);
+  const double ne = __shfl_sync(NX_FULL, acc, src);
   const double y2 = static_cast<double>(n);
   const double prior[5] = {cur.tau0, cur.w0, cur.ws, cur.tauB, cur.tauS};
   double x[5];
-  bool ok;
-  {
-    double a[5][5], bb[5];
-#pragma unroll
-    for (int i = 0; i < 5; ++i) {
-      bb[i] = atb[i];
-#pragma unroll
-      for (int j = 0; j < 5; ++j) a[i][j] = ata[i][j];
-    }
-    ok = solve5(a, bb, x);
-  }
+  bool ok = solve5_warp(ne, x);
   if (ok) {
     // noise_level = 8 * rel_sse(x), exact left fold over <= short_window rows
     double run = 0.0;
@@ -228,22 +258,7 @@ __device__ bool update_linear(Ctx& c, int e) {
     const double den = (y2 < 1e-30) ? 1e-30 : y2;
     const double v = noise / den;
     const double lambda = (v < 1e-2) ? v : 1e-2;
-    if (lambda > 1e-14) {
-      double a[5][5], bb[5];
-#pragma unroll
-      for (int i = 0; i < 5; ++i) {
-        bb[i] = atb[i];
-#pragma unroll
-        for (int j = 0; j < 5; ++j) a[i][j] = ata[i][j];
-      }
-#pragma unroll
-      for (int i = 0; i < 5; ++i) {
-        const double d = lambda * ata[i][i];
-        a[i][i] += d;
-        bb[i] += d * prior[i];
-      }
-      ok = solve5(a, bb, x);
-    }
+    if (lambda > 1e-14) ok = solve5_warp(ridge_elem(ne, lambda, prior), x);
   }
   if (!ok) {
     // Degenerate design: rescale the linear tier (learner.cpp:304-333).
@@ -428,30 +443,29 @@ __device__ double sse_x_exact(Ctx& c, const Stage& S, double kB, double kS, cons
   return __shfl_sync(NX_FULL, run, 0);
 }
 
-struct Normal {  // assembled normal equations of one fit
-  double A[5][5], t[5], y2;
-};
 
 // SSE(x) = y2 - 2 x.t + x^T A x with its absolute rounding bound: accumulation
 // error of every entry (all terms positive) plus the closed-form arithmetic,
 // plus the per-term gap between x.row and the reference's model evaluation.
-__device__ void closed_sse(const Normal& N, const double x[5], int n, double& val, double& bound) {
-  double lin = 0.0, lin_abs = 0.0, quad = 0.0, quad_abs = 0.0;
-#pragma unroll
-  for (int i = 0; i < 5; ++i) {
-    lin += x[i] * N.t[i];
-    lin_abs += fabs(x[i]) * N.t[i];
-#pragma unroll
-    for (int j = 0; j < 5; ++j) {
-      quad += x[i] * x[j] * N.A[i][j];
-      quad_abs += fabs(x[i]) * fabs(x[j]) * N.A[i][j];
-    }
+__device__ void closed_sse(double e, const double x[5], int n, double y2, double& val,
+                           double& bound) {
+  const int lane = lane_id();
+  double q = 0.0, qa = 0.0, l = 0.0, la = 0.0;
+  if (lane < 25) {
+    const double xi = pick5(x, lane / 5), xj = pick5(x, lane % 5);
+    q = xi * xj * e;
+    qa = fabs(xi) * fabs(xj) * e;
+  } else if (lane < 30) {
+    const double xi = pick5(x, lane - 25);
+    l = xi * e;
+    la = fabs(xi) * e;
   }
-  val = N.y2 - 2.0 * lin + quad;
-  const double M = N.y2 + 2.0 * lin_abs + quad_abs;
-  const double s = val > 0.0 ? val : 0.0;
+  const double quad = warp_sum(q), quad_abs = warp_sum(qa), lin = warp_sum(l), lin_abs = warp_sum(la);
+  val = y2 - 2.0 * lin + quad;
+  const double M = y2 + 2.0 * lin_abs + quad_abs;
+  const double sv = val > 0.0 ? val : 0.0;
   bound = 2.0 * (static_cast<double>(n) + 64.0) * kU * M +
-          32.0 * kU * (sqrt(static_cast<double>(n) * (s + 1.0)) + s) + 1e-300;
+          32.0 * kU * (sqrt(static_cast<double>(n) * (sv + 1.0)) + sv) + 1e-300;
 }
 
 // Per-update staging: chronological copy, gate statistics, invariant sums.
@@ -531,11 +545,20 @@ struct FitOut {
 };
 
 // gauged_fit (learner.cpp:228-298) for fixed (kB, kS).
+__device__ FitOut gauged_fit_impl(Ctx& c, Stage& S, const Params& cur, double kB, double kS);
 __device__ FitOut gauged_fit(Ctx& c, Stage& S, const Params& cur, double kB, double kS) {
-  if (c.lane == 0) c.rs->work[5] += 1;
+  const long long t0 = nx_clock();
+  FitOut o = gauged_fit_impl(c, S, cur, kB, kS);
+  if (c.lane == 0) count(c.rs->cycles[10], nx_clock() - t0);
+  return o;
+}
+__device__ FitOut gauged_fit_impl(Ctx& c, Stage& S, const Params& cur, double kB, double kS) {
+  if (c.lane == 0) count(c.rs->work[5], 1);
   const int n = S.n;
+  const long long tf0 = nx_clock();
   if (kB != S.ifb_k) {
     __syncwarp();
+#pragma unroll 4
     for (int b = 1 + c.lane; b <= S.tab; b += 32)
       S.ifb[b] = 1.0 / raw_factor(kB, static_cast<double>(b));
     S.ifb_k = kB;
@@ -544,12 +567,15 @@ __device__ FitOut gauged_fit(Ctx& c, Stage& S, const Params& cur, double kB, dou
   const bool new_s = kS != S.ifs_k;
   if (new_s && S.use_tab) {
     __syncwarp();
+#pragma unroll 4
     for (int k = c.lane; k < S.U; k += 32) {
       const int sv = S.us[k];
       S.stab[sv] = 1.0 / raw_factor(kS, static_cast<double>(sv));
     }
     __syncwarp();
   }
+  const long long tf1 = nx_clock();
+  if (c.lane == 0) count(c.rs->cycles[7], tf1 - tf0);
   double a01 = 0, a02 = 0, a11 = 0, a12 = 0, a22 = 0, a13 = 0, a14 = 0, a23 = 0, a24 = 0;
   double t1 = 0, t2 = 0;
   auto accumulate = [&](double iy, int bi, int si, double ifs) {
@@ -604,60 +630,53 @@ __device__ FitOut gauged_fit(Ctx& c, Stage& S, const Params& cur, double kB, dou
     }
   }
   S.ifs_k = kS;
-  Normal N;
-  N.A[0][0] = S.A00; N.A[0][3] = N.A[3][0] = S.A03; N.A[0][4] = N.A[4][0] = S.A04;
-  N.A[3][3] = S.A33; N.A[3][4] = N.A[4][3] = S.A34; N.A[4][4] = S.A44;
-  N.A[0][1] = N.A[1][0] = warp_sum(a01);
-  N.A[0][2] = N.A[2][0] = warp_sum(a02);
-  N.A[1][1] = warp_sum(a11);
-  N.A[1][2] = N.A[2][1] = warp_sum(a12);
-  N.A[2][2] = warp_sum(a22);
-  N.A[1][3] = N.A[3][1] = warp_sum(a13);
-  N.A[1][4] = N.A[4][1] = warp_sum(a14);
-  N.A[2][3] = N.A[3][2] = warp_sum(a23);
-  N.A[2][4] = N.A[4][2] = warp_sum(a24);
-  N.t[0] = S.t0; N.t[1] = warp_sum(t1); N.t[2] = warp_sum(t2); N.t[3] = S.t3; N.t[4] = S.t4;
-  N.y2 = static_cast<double>(n);  // sum of 1.0 * 1.0 (learner.cpp:73)
+  if (c.lane == 0) count(c.rs->cycles[9], nx_clock() - tf1);
+  const long long tf2 = nx_clock();
+  const double u15[15] = {S.A00, warp_sum(a01), warp_sum(a02), S.A03, S.A04,
+                          warp_sum(a11), warp_sum(a12), warp_sum(a13), warp_sum(a14),
+                          warp_sum(a22), warp_sum(a23), warp_sum(a24), S.A33, S.A34, S.A44};
+  const double t5[5] = {S.t0, warp_sum(t1), warp_sum(t2), S.t3, S.t4};
+  const double e = normal_elem(u15, t5);
+  const double y2 = static_cast<double>(n);  // sum of 1.0 * 1.0 (learner.cpp:73)
   const double prior[5] = {cur.tau0, cur.w0 / cur.p_max, cur.ws / cur.p_max, cur.tauB, cur.tauS};
   FitOut out;
   out.err = __longlong_as_double(0x7ff0000000000000LL);
   out.bound = 0.0;
   double x[5];
-  {
-    double a[5][5], bb[5];
-#pragma unroll
-    for (int i = 0; i < 5; ++i) {
-      bb[i] = N.t[i];
-#pragma unroll
-      for (int j = 0; j < 5; ++j) a[i][j] = N.A[i][j];
-    }
-    if (!solve5(a, bb, x)) return out;
-  }
+  if (!solve5_warp(e, x)) return out;
   // lambda = min(1e-7, sse(x) / max(y2, 1e-30))  (learner.cpp:84-85, cap 1e-7)
-  const double den = (N.y2 < 1e-30) ? 1e-30 : N.y2;
-  double sv, sb;
-  closed_sse(N, x, n, sv, sb);
+  const double den = (y2 < 1e-30) ? 1e-30 : y2;
+  // Certify sse(x) / den >= 1e-7 (=> lambda = cap) from a lower bound: the
+  // sum has non-negative terms, so 32 of them evaluated directly (one per
+  // lane, the reference's per-term formula) bound the left-fold total from
+  // below; the closed form backs it up, the exact fold decides the rest.
+  double lb;
+  {
+    const int i = c.lane * (n / 32);
+    double rr = 0.0;
+    if (i < n) {
+      const double b = S.sb[i], s = S.ss[i], y = S.sy[i];
+      double f = raw_factor(kB, b) * raw_factor(kS, s);
+      f = (f < 1e-300) ? 1e-300 : f;
+      double pred = 0.0;
+      pred += 1.0 * x[0];
+      pred += (1.0 / f) * x[1];
+      pred += (s / f) * x[2];
+      pred += b * x[3];
+      pred += s * x[4];
+      const double r = (y - pred) / y;
+      rr = r * r;
+    }
+    lb = warp_sum(rr) * (1.0 - 1e-6);
+  }
+  double sv = 0.0, sb = 0.0;
+  if (!(lb / den > 1e-7 * (1.0 + 8.0 * kU))) closed_sse(e, x, n, y2, sv, sb);
   double lambda = 1e-7;
-  if (!((sv - sb) / den > 1e-7 * (1.0 + 8.0 * kU))) {
+  if (!(lb / den > 1e-7 * (1.0 + 8.0 * kU)) && !((sv - sb) / den > 1e-7 * (1.0 + 8.0 * kU))) {
     const double v = sse_x_exact(c, S, kB, kS, x) / den;
     lambda = (v < 1e-7) ? v : 1e-7;
   }
-  if (lambda > 1e-14) {
-    double a[5][5], bb[5];
-#pragma unroll
-    for (int i = 0; i < 5; ++i) {
-      bb[i] = N.t[i];
-#pragma unroll
-      for (int j = 0; j < 5; ++j) a[i][j] = N.A[i][j];
-    }
-#pragma unroll
-    for (int i = 0; i < 5; ++i) {
-      const double d = lambda * N.A[i][i];
-      a[i][i] += d;
-      bb[i] += d * prior[i];
-    }
-    if (!solve5(a, bb, x)) return out;
-  }
+  if (lambda > 1e-14 && !solve5_warp(ridge_elem(e, lambda, prior), x)) return out;
   const double tau0 = x[0] < 0.0 ? 0.0 : x[0];
   const double aa = x[1] < 0.0 ? 0.0 : x[1];
   const double slope = cur.ws / cur.p_max + cur.tauS;
@@ -678,13 +697,21 @@ __device__ FitOut gauged_fit(Ctx& c, Stage& S, const Params& cur, double kB, dou
   p.tauS = x[4] < 0.0 ? 0.0 : x[4];
   out.p = p;
   const double xp[5] = {p.tau0, aa, cc, p.tauB, p.tauS};  // T(p) == xp . row
-  closed_sse(N, xp, n, out.err, out.bound);
+  closed_sse(e, xp, n, y2, out.err, out.bound);
+  if (c.lane == 0) count(c.rs->cycles[13], nx_clock() - tf2);
   return out;
 }
 
 // Certified "exact(a) < exact(b) * f" for two windowed-SSE intervals; exact
 // re-evaluation only when the intervals cannot decide.
+__device__ bool less_scaled_impl(Ctx& c, const Stage& S, const FitOut& a, const FitOut& b, double f);
 __device__ bool less_scaled(Ctx& c, const Stage& S, const FitOut& a, const FitOut& b, double f) {
+  const long long t0 = nx_clock();
+  const bool r = less_scaled_impl(c, S, a, b, f);
+  if (c.lane == 0) count(c.rs->cycles[11], nx_clock() - t0);
+  return r;
+}
+__device__ bool less_scaled_impl(Ctx& c, const Stage& S, const FitOut& a, const FitOut& b, double f) {
   const double a_hi = a.err + a.bound, a_lo = a.err - a.bound;
   const double b_hi = (b.err + b.bound) * f, b_lo = (b.err - b.bound) * f;
   if (a_hi < b_lo * (1.0 - 4.0 * kU)) return true;
@@ -701,19 +728,23 @@ __device__ void update_structural(Ctx& c, int e) {
   Stage S = stage_of(c);
   bool saturated;
   int shaped, bmax;
+  const long long ts0 = nx_clock();
   stage_window(c, w, cur, S, saturated, shaped, bmax);
+  if (c.lane == 0) count(c.rs->cycles[12], nx_clock() - ts0);
   if (saturated || shaped < 16) {
     __syncwarp();
     if (c.lane == 0) g.cnt[6] += 1;
     __syncwarp();
     return;
   }
-  if (c.lane == 0) c.rs->work[4] += n;
+  if (c.lane == 0) count(c.rs->work[4], n);
   // base_err: direct evaluation, tree order; tree vs left fold of n positive
   // terms differ by at most 2(n-1)u of the sum
   FitOut base;
   base.p = cur;
+  const long long tb0 = nx_clock();
   base.err = wsse_tree(c, S, cur);
+  if (c.lane == 0) count(c.rs->cycles[14], nx_clock() - tb0);
   base.bound = 2.0 * (static_cast<double>(n) + 2.0) * kU * base.err;
   const double lo = log(1e-8), hi = log(1e4);
   const double shrink = 1.0 - 1e-3;
@@ -783,9 +814,76 @@ __device__ void update_structural(Ctx& c, int e) {
   update_linear(c, e);
 }
 
+// Queue a structural refit of engine e for the refit warp. The engine's
+// learner state (params, ring, counters) is frozen until the refit clears
+// refit_pending: the event loop waits (wait_refit) before its next read.
+__device__ void post_refit(Ctx& c, int e) {
+  __syncwarp();
+  if (c.lane == 0) {
+    vstore(c.eng[e].refit_pending, 1);
+    const int t = vload(c.rs->jq_tail);
+    c.rs->jq_eng[t & 63] = e;
+    __threadfence_block();
+    vstore(c.rs->jq_tail, t + 1);
+  }
+  __syncwarp();
+}
+
+// Tells the refit warp the replica is done (job id -1).
+__device__ void post_exit(Ctx& c) {
+  __syncwarp();
+  if (c.lane == 0) {
+    const int t = vload(c.rs->jq_tail);
+    c.rs->jq_eng[t & 63] = -1;
+    __threadfence_block();
+    vstore(c.rs->jq_tail, t + 1);
+  }
+  __syncwarp();
+}
+
+__device__ void wait_refit(Ctx& c, int e) {
+  if (!vload(c.eng[e].refit_pending)) return;
+  const long long t0 = nx_clock();
+  while (vload(c.eng[e].refit_pending)) __nanosleep(64);
+  __threadfence_block();
+  __syncwarp();
+  if (c.lane == 0) count(c.rs->cycles[8], nx_clock() - t0);
+}
+
+// The refit warp: pops engine ids and runs update_structural until it pops -1.
+__device__ void refit_worker(Ctx& c) {
+  while (true) {
+    int e = -2;
+    if (c.lane == 0) {
+      const int h = vload(c.rs->jq_head);
+      while (vload(c.rs->jq_tail) == h) __nanosleep(128);
+      __threadfence_block();
+      e = *reinterpret_cast<const volatile int32_t*>(&c.rs->jq_eng[h & 63]);
+    }
+    e = __shfl_sync(NX_FULL, e, 0);
+    if (e < 0) {
+      if (c.lane == 0) vstore(c.rs->jq_head, vload(c.rs->jq_head) + 1);
+      __syncwarp();
+      return;
+    }
+    {
+      PhaseTimer pt(c.rs, 6);
+      update_structural(c, e);
+    }
+    __threadfence_block();
+    __syncwarp();
+    if (c.lane == 0) {
+      vstore(c.eng[e].refit_pending, 0);
+      vstore(c.rs->jq_head, vload(c.rs->jq_head) + 1);
+    }
+    __syncwarp();
+  }
+}
+
 // record_sample (learner.cpp:130-146): ring push + periodic refits.
 __device__ void record_sample(Ctx& c, int e, int b, int s, double y) {
   EngSm& g = c.eng[e];
+  wait_refit(c, e);
   if (!(y > 0.0) || !(b >= 1 && s >= b)) {
     fail(c, 1, NX_SITE_SAMPLE, b);
     return;
@@ -813,10 +911,7 @@ __device__ void record_sample(Ctx& c, int e, int b, int s, double y) {
     PhaseTimer pt(c.rs, 5);
     update_linear(c, e);
   }
-  if (seen >= c.d->min_s && seen % c.d->s_period == 0) {
-    PhaseTimer pt(c.rs, 6);
-    update_structural(c, e);
-  }
+  if (seen >= c.d->min_s && seen % c.d->s_period == 0) post_refit(c, e);
 }
 
 }  // namespace nxd

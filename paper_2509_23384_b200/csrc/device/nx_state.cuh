@@ -35,6 +35,7 @@ struct EngSm {
   int32_t learn_b, learn_s;
   int32_t ring_size, ring_head, tw_head, tw_len, dq_head, dq_len, lat_head, lat_len;
   int32_t has_rep, noise_pos;
+  int32_t refit_pending;                       // structural refit queued / running
 };
 
 struct RepSm {
@@ -42,10 +43,12 @@ struct RepSm {
   uint64_t next_arr;                           // arrival time at the cursor (cached)
   int64_t arrived, rejected, pending, n_rec, events, info;
   int64_t work[6];
-  int64_t cycles[8];
+  int64_t cycles[16];
   double l_bar_ema;
   uint32_t next_seq;
   int32_t cursor, status, site;
+  int32_t jq_head, jq_tail;                    // structural-refit job ring (warp 0 -> warp 1)
+  int32_t jq_eng[64];
 };
 
 struct Ctx {
@@ -57,8 +60,10 @@ struct Ctx {
   int32_t* prefix;         // LENS prefix sums (union with chunk)
   double* chunk;           // 32 x 5 staging rows for exact-order folds
   double* scratch;         // learner scratch in HBM (fs cache, fb table, rows)
+  double* lin_rows;        // this warp's linear-tier row buffer in the scratch
   int64_t roff, soff;
   int n_eng, n_req, n_sess, lane, prefix_cap;
+  int worker;              // 0: event-loop warp, 1: structural-refit warp
 };
 
 template <class T>
@@ -95,8 +100,21 @@ struct PhaseTimer {
   long long t0;
   __device__ __forceinline__ PhaseTimer(RepSm* r, int kk) : rs(r), k(kk), t0(nx_clock()) {}
   __device__ __forceinline__ ~PhaseTimer() {
-    if (lane_id() == 0) rs->cycles[k] += nx_clock() - t0;
+    if (lane_id() == 0)
+      atomicAdd(reinterpret_cast<unsigned long long*>(&rs->cycles[k]),
+                static_cast<unsigned long long>(nx_clock() - t0));
   }
 };
+
+// counters shared by both warps of a replica CTA
+__device__ __forceinline__ void count(int64_t& slot, int64_t v) {
+  atomicAdd(reinterpret_cast<unsigned long long*>(&slot), static_cast<unsigned long long>(v));
+}
+__device__ __forceinline__ int32_t vload(const int32_t& x) {
+  return *reinterpret_cast<const volatile int32_t*>(&x);
+}
+__device__ __forceinline__ void vstore(int32_t& x, int32_t v) {
+  *reinterpret_cast<volatile int32_t*>(&x) = v;
+}
 
 }  // namespace nxd

@@ -343,6 +343,7 @@ __device__ void try_begin_step(Ctx& c, int e, int64_t now_us) {
   EngSm& g = c.eng[e];
   __syncwarp();
   if (g.busy || (g.wq_len == 0 && g.rq_len == 0)) return;
+  wait_refit(c, e);  // planning reads the learner's params
   PhaseTimer pt(c.rs, 2);
   const NxEngineDesc& ed = c.ed[e];
   if (ed.policy == 0) plan_lens(c, e);
@@ -662,6 +663,7 @@ __device__ void step_complete(Ctx& c, int e, int64_t now_us) {
 __device__ void state_report(Ctx& c, int e, int64_t now_us) {
   EngSm& g = c.eng[e];
   const NxEngineDesc& ed = c.ed[e];
+  wait_refit(c, e);  // the report exports the learner's p_max
   __syncwarp();
   if (c.lane == 0) {
     const double now = to_ms(now_us);
@@ -936,7 +938,7 @@ __device__ void init_replica(Ctx& c) {
     g.learn_b = 0; g.learn_s = 0;
     g.ring_size = 0; g.ring_head = 0; g.tw_head = 0; g.tw_len = 0;
     g.dq_head = 0; g.dq_len = 0; g.lat_head = 0; g.lat_len = 0; g.has_rep = 0;
-    g.dq_t0 = kNoEvent; g.dq_s0 = 0; g.noise_pos = 32;
+    g.dq_t0 = kNoEvent; g.dq_s0 = 0; g.noise_pos = 32; g.refit_pending = 0;
   }
   if (c.lane == 0) {
     RepSm& R = *c.rs;
@@ -945,7 +947,9 @@ __device__ void init_replica(Ctx& c) {
     for (int i = 0; i < 4; ++i) R.rng[i] = d.router_rng[i];
     R.arrived = 0; R.rejected = 0; R.pending = c.n_req; R.n_rec = 0; R.events = 0; R.info = 0;
     for (int i = 0; i < 6; ++i) R.work[i] = 0;
-    for (int i = 0; i < 8; ++i) R.cycles[i] = 0;
+    for (int i = 0; i < 16; ++i) R.cycles[i] = 0;
+    R.jq_head = 0;
+    R.jq_tail = 0;
     R.l_bar_ema = 128.0;
     R.next_seq = static_cast<uint32_t>(c.n_eng + c.n_req);  // arrival i carries seq E + i
     R.cursor = 0; R.status = 0; R.site = 0;
@@ -955,7 +959,6 @@ __device__ void init_replica(Ctx& c) {
 }
 
 __device__ void run_replica(Ctx& c) {
-  init_replica(c);
   const NxReplicaDesc& d = *c.d;
   const uint64_t duration = static_cast<uint64_t>(d.duration_us);
   while (!failed(c)) {
@@ -1111,7 +1114,7 @@ __device__ void write_outputs(Ctx& c, int r) {
     o.err_site = R.site;
     o.err_info = R.info;
     for (int i = 0; i < 6; ++i) o.work[i] = R.work[i];
-    for (int i = 0; i < 8; ++i) o.cycles[i] = R.cycles[i];
+    for (int i = 0; i < 16; ++i) o.cycles[i] = R.cycles[i];
   }
   for (int e = c.lane; e < c.n_eng; e += 32) {
     const EngSm& g = c.eng[e];
@@ -1129,30 +1132,34 @@ __device__ void write_outputs(Ctx& c, int r) {
 
 }  // namespace nxd
 
-// One warp per replica; warps pull replica indices (in host-chosen order,
-// longest first) from a global counter so a long replica never blocks a block.
-extern "C" __global__ void __launch_bounds__(128)
+// One CTA of two warps per replica: warp 0 runs the event loop, warp 1 runs
+// the queued structural refits. CTAs pull replica indices (host order, longest
+// expected first) from a global counter so a long replica never idles others.
+extern "C" __global__ void __launch_bounds__(64)
 nx_sim_kernel(const NxPools* __restrict__ pools, const int32_t* __restrict__ order, int n_rep,
-              int* next_rep, int smem_per_warp, int prefix_cap) {
+              int* next_rep, int smem_per_cta, int prefix_cap) {
   using namespace nxd;
   extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ int s_slot;
   const int warp = threadIdx.x >> 5;
-  unsigned char* base = smem + static_cast<size_t>(warp) * smem_per_warp;
   Ctx c;
   c.P = pools;
   c.lane = lane_id();
-  c.rs = reinterpret_cast<RepSm*>(base);
+  c.worker = warp;
+  c.rs = reinterpret_cast<RepSm*>(smem);
   const size_t rep_bytes = (sizeof(RepSm) + 15) & ~size_t(15);
-  c.chunk = reinterpret_cast<double*>(base + rep_bytes);
-  c.prefix = reinterpret_cast<int32_t*>(base + rep_bytes);
   const size_t stage = ((static_cast<size_t>(prefix_cap) * 4 > 32 * 5 * 8 ? static_cast<size_t>(prefix_cap) * 4
                                                                         : 32 * 5 * 8) + 15) & ~size_t(15);
-  c.eng = reinterpret_cast<EngSm*>(base + rep_bytes + stage);
+  c.chunk = reinterpret_cast<double*>(smem + rep_bytes + warp * stage);
+  c.prefix = reinterpret_cast<int32_t*>(c.chunk);
+  c.eng = reinterpret_cast<EngSm*>(smem + rep_bytes + 2 * stage);
   c.prefix_cap = prefix_cap;
+  (void)smem_per_cta;
   while (true) {
-    int slot = 0;
-    if (c.lane == 0) slot = atomicAdd(next_rep, 1);
-    slot = __shfl_sync(NX_FULL, slot, 0);
+    if (threadIdx.x == 0) s_slot = atomicAdd(next_rep, 1);
+    __syncthreads();
+    const int slot = s_slot;
+    __syncthreads();
     if (slot >= n_rep) break;
     const int r = order[slot];
     c.d = pools->rep + r;
@@ -1163,24 +1170,35 @@ nx_sim_kernel(const NxPools* __restrict__ pools, const int32_t* __restrict__ ord
     c.roff = c.d->req_off;
     c.soff = c.d->sess_off;
     c.scratch = pools->scratch + c.d->scratch_off;
-    run_replica(c);
-    write_outputs(c, r);
+    c.lin_rows = c.scratch + 6 * c.d->long_w + kFbTable + warp * c.d->long_w;
+    if (warp == 0) init_replica(c);
+    __syncthreads();
+    if (warp == 0) {
+      run_replica(c);
+      for (int e = 0; e < c.n_eng; ++e) wait_refit(c, e);
+      post_exit(c);
+    } else {
+      refit_worker(c);
+    }
+    __syncthreads();
+    if (warp == 0) write_outputs(c, r);
+    __syncthreads();
   }
 }
 
-// Size of the per-warp shared-memory slice (host uses the same formula).
+// Size of the per-CTA shared-memory slice (host uses the same formula).
 extern "C" size_t nx_sim_smem_per_warp(int max_engines, int prefix_cap) {
   using namespace nxd;
   const size_t rep_bytes = (sizeof(RepSm) + 15) & ~size_t(15);
   const size_t stage = ((static_cast<size_t>(prefix_cap) * 4 > 32 * 5 * 8 ? static_cast<size_t>(prefix_cap) * 4
                                                                         : 32 * 5 * 8) + 15) & ~size_t(15);
-  return rep_bytes + stage + sizeof(EngSm) * static_cast<size_t>(max_engines);
+  return rep_bytes + 2 * stage + sizeof(EngSm) * static_cast<size_t>(max_engines);
 }
 
 extern "C" cudaError_t nx_launch_sim(const NxPools* d_pools, const int32_t* d_order, int n_rep,
                                      int* d_next, int smem_per_warp, int prefix_cap, int grid,
                                      int warps_per_block, cudaStream_t st) {
-  const size_t smem = static_cast<size_t>(smem_per_warp) * warps_per_block;
+  const size_t smem = static_cast<size_t>(smem_per_warp);  // one replica per CTA
   cudaError_t err = cudaFuncSetAttribute(nx_sim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
   if (err != cudaSuccess) return err;

@@ -83,7 +83,7 @@ struct Arena {
   }
 };
 
-constexpr int kWarpsPerBlock = 4;
+constexpr int kWarpsPerBlock = 2;  // event-loop warp + refit warp per replica CTA
 
 }  // namespace
 
@@ -473,11 +473,11 @@ int nx_sim_launch(nx_sim_t h) {
     cuda_check(cudaMemsetAsync(h->d_arena + h->off_ff_begin, 0xff,
                                h->off_ff_end - h->off_ff_begin, st), "memset state");
     const int spw = static_cast<int>(nx_sim_smem_per_warp(h->max_eng, h->prefix_cap));
-    const size_t smem = static_cast<size_t>(spw) * kWarpsPerBlock;
+    const size_t smem = static_cast<size_t>(spw);  // per replica CTA
     int per_sm = 0;
     cuda_check(nx_sim_occupancy(kWarpsPerBlock, smem, &per_sm), "occupancy");
     if (per_sm < 1) throw NxError(NX_ECUDA, "simulation kernel does not fit on an SM");
-    const int need = (h->n_rep + kWarpsPerBlock - 1) / kWarpsPerBlock;
+    const int need = h->n_rep;
     const int grid = std::max(1, std::min(need, per_sm * sm_count(h->device)));
     cuda_check(cudaEventRecord(h->ev0, st), "event");
     cuda_check(nx_launch_sim(h->d_pools, h->d_order, h->n_rep, h->d_next, spw, h->prefix_cap, grid,
@@ -645,10 +645,10 @@ int nx_sim_work(nx_sim_t h, int32_t replica, int64_t* out6) {
   });
 }
 
-int nx_sim_phase_cycles(nx_sim_t h, int32_t replica, int64_t* out8) {
+int nx_sim_phase_cycles(nx_sim_t h, int32_t replica, int64_t* out10) {
   return guard([&] {
     if (replica < 0 || replica >= h->n_rep) throw std::invalid_argument("replica out of range");
-    for (int i = 0; i < 8; ++i) out8[i] = h->h_rep_out[replica].cycles[i];
+    for (int i = 0; i < 16; ++i) out10[i] = h->h_rep_out[replica].cycles[i];
   });
 }
 

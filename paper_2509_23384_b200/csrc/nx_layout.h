@@ -62,8 +62,9 @@ typedef struct NxReplicaOut {
   /* SM cycles spent per phase (clock64, lane 0): [0] event selection + hash,
      [1] routing + admission, [2] step planning (LENS / baseline, KV trim,
      oracle), [3] step completion, [4] state reports, [5] linear refits,
-     [6] structural refits, [7] report deliveries */
-  int64_t cycles[8];
+     [6] structural refits (refit warp, overlapped), [7] report deliveries,
+     [8] event-loop warp blocked on a pending refit, [9]-[15] refit internals */
+  int64_t cycles[16];
 } NxReplicaOut;
 
 typedef struct NxEngineOut {

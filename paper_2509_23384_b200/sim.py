@@ -105,7 +105,7 @@ class Batch:
         return list(out)
 
     def phase_cycles(self, r: int):
-        out = (C.c_int64 * 8)()
+        out = (C.c_int64 * 16)()
         check(lib().nx_sim_phase_cycles(self.h, r, out))
         return list(out)
 

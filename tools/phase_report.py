@@ -3,7 +3,7 @@ import argparse, sys
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2509_23384_b200 import sim, workloads as W
-NAMES = ["select+hash", "route+admit", "plan(LENS)", "complete", "report", "linear", "structural", "deliver"]
+NAMES = ["select+hash", "route+admit", "plan(LENS)", "complete", "report", "linear", "structural*", "fit-tables", "refit-wait", "fit-pass", "fit-total", "less_scaled", "stage", "fit-solve", "base-err", "-"]
 ap = argparse.ArgumentParser()
 ap.add_argument("--requests", type=int, default=2000)
 a = ap.parse_args()
@@ -12,7 +12,7 @@ b = sim.Batch(cfgs)
 b.run()
 print(f"kernel {b.kernel_ms():.1f} ms for {len(cfgs)} replicas")
 for i, c in enumerate(cfgs):
-    cyc = b.phase_cycles(i); tot = sum(cyc)
+    cyc = b.phase_cycles(i); tot = sum(cyc[:9]) - cyc[6] - cyc[7]  # refit-warp phases overlap
     s = b.summaries()[i]; w = b.work(i)
     print(f"rate {c['workload']['rate']:5.1f} {c['router']['policy']:12s} events {s.events:7d} dec {s.decisions:7d} "
           f"total {tot/1.9e9:6.3f}s  cyc/event {tot/max(1,s.events):7.0f}  steps {w[0]} fits {w[5]}")

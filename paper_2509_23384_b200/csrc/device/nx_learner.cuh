@@ -32,73 +32,92 @@ __device__ __forceinline__ double pick5(const double v[5], int k) {
   return r;
 }
 
-__device__ bool solve5_warp(double v, double x[5]) {
+// K independent systems in lockstep: their shuffle and division latencies
+// overlap. ok[k] reports each system's rank test separately.
+template <int K>
+__device__ void solve5_warp_k(double (&v)[K], double (&x)[K][5], bool (&ok)[K]) {
   const int lane = lane_id();
   const bool isA = lane < 25;
   const int i = isA ? lane / 5 : (lane < 30 ? lane - 25 : 0);
   const int j = isA ? lane % 5 : 5;
-  // column scaling (max is exact in any order)
-  double m = 0.0;
+  double sc[K][5], norm[K];
 #pragma unroll
-  for (int r = 0; r < 5; ++r) m = dmax(m, fabs(__shfl_sync(NX_FULL, v, r * 5 + (j < 5 ? j : 0))));
-  const bool zero_col = __any_sync(NX_FULL, isA && i == 0 && m <= 0.0);
-  if (zero_col) return false;
-  const double scale = isA ? 1.0 / m : 1.0;
-  if (isA) v *= scale;
-  double sc[5];
+  for (int k = 0; k < K; ++k) {
+    double m = 0.0;
 #pragma unroll
-  for (int q = 0; q < 5; ++q) sc[q] = __shfl_sync(NX_FULL, scale, q);
-  double norm = isA ? fabs(v) : 0.0;
+    for (int r = 0; r < 5; ++r)
+      m = dmax(m, fabs(__shfl_sync(NX_FULL, v[k], r * 5 + (j < 5 ? j : 0))));
+    ok[k] = !__any_sync(NX_FULL, isA && i == 0 && m <= 0.0);
+    const double scale = (isA && m > 0.0) ? 1.0 / m : 1.0;
+    if (isA) v[k] *= scale;
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) norm = dmax(norm, __shfl_xor_sync(NX_FULL, norm, o));
+    for (int q = 0; q < 5; ++q) sc[k][q] = __shfl_sync(NX_FULL, scale, q);
+    double nm = isA ? fabs(v[k]) : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) nm = dmax(nm, __shfl_xor_sync(NX_FULL, nm, o));
+    norm[k] = nm;
+  }
 #pragma unroll
   for (int col = 0; col < 5; ++col) {
-    double cv[5];
 #pragma unroll
-    for (int r = 0; r < 5; ++r) cv[r] = fabs(__shfl_sync(NX_FULL, v, r * 5 + col));
-    int piv = col;
-    double pv = cv[col];
+    for (int k = 0; k < K; ++k) {
+      double cv[5];
 #pragma unroll
-    for (int r = col + 1; r < 5; ++r)
-      if (cv[r] > pv) {
-        piv = r;
-        pv = cv[r];
+      for (int r = 0; r < 5; ++r) cv[r] = fabs(__shfl_sync(NX_FULL, v[k], r * 5 + col));
+      int piv = col;
+      double pv = cv[col];
+#pragma unroll
+      for (int r = col + 1; r < 5; ++r)
+        if (cv[r] > pv) {
+          piv = r;
+          pv = cv[r];
+        }
+      if (pv < 1e-10 * norm[k]) ok[k] = false;
+      int src = lane;
+      if (lane < 30) {
+        const int base = isA ? 0 : 25, stride = isA ? 5 : 1, off = isA ? j : 0;
+        if (i == col) src = base + piv * stride + off;
+        else if (i == piv) src = base + col * stride + off;
       }
-    if (pv < 1e-10 * norm) return false;
-    // swap rows col <-> piv (A and b lanes alike)
-    int src = lane;
-    if (lane < 30) {
-      const int base = isA ? 0 : 25, stride = isA ? 5 : 1, off = isA ? j : 0;
-      if (i == col) src = base + piv * stride + off;
-      else if (i == piv) src = base + col * stride + off;
-    }
-    v = __shfl_sync(NX_FULL, v, src);
-    const double diag = __shfl_sync(NX_FULL, v, col * 5 + col);
-    const double pivrow = __shfl_sync(NX_FULL, v, isA ? col * 5 + j : 25 + col);
-    const double arc = __shfl_sync(NX_FULL, v, i * 5 + col);
-    if (lane < 30 && i > col && (j >= col)) {
-      const double f = arc / diag;
-      v -= f * pivrow;
+      v[k] = __shfl_sync(NX_FULL, v[k], src);
+      const double diag = __shfl_sync(NX_FULL, v[k], col * 5 + col);
+      const double pivrow = __shfl_sync(NX_FULL, v[k], isA ? col * 5 + j : 25 + col);
+      const double arc = __shfl_sync(NX_FULL, v[k], i * 5 + col);
+      if (lane < 30 && i > col && j >= col) {
+        const double f = arc / diag;
+        v[k] -= f * pivrow;
+      }
     }
   }
-  // back substitution (serial order), then undo the column scaling
-  double u[5][5], bb[5];
 #pragma unroll
-  for (int r = 0; r < 5; ++r) {
+  for (int k = 0; k < K; ++k) {
+    double u[5][5], bb[5];
 #pragma unroll
-    for (int q = r; q < 5; ++q) u[r][q] = __shfl_sync(NX_FULL, v, r * 5 + q);
-    bb[r] = __shfl_sync(NX_FULL, v, 25 + r);
+    for (int r = 0; r < 5; ++r) {
+#pragma unroll
+      for (int q = r; q < 5; ++q) u[r][q] = __shfl_sync(NX_FULL, v[k], r * 5 + q);
+      bb[r] = __shfl_sync(NX_FULL, v[k], 25 + r);
+    }
+#pragma unroll
+    for (int r = 4; r >= 0; --r) {
+      double acc = bb[r];
+#pragma unroll
+      for (int q = r + 1; q < 5; ++q) acc -= u[r][q] * x[k][q];
+      x[k][r] = acc / u[r][r];
+    }
+#pragma unroll
+    for (int q = 0; q < 5; ++q) x[k][q] *= sc[k][q];
   }
+}
+
+__device__ __forceinline__ bool solve5_warp(double v, double x[5]) {
+  double vv[1] = {v};
+  double xx[1][5];
+  bool ok[1];
+  solve5_warp_k<1>(vv, xx, ok);
 #pragma unroll
-  for (int r = 4; r >= 0; --r) {
-    double acc = bb[r];
-#pragma unroll
-    for (int q = r + 1; q < 5; ++q) acc -= u[r][q] * x[q];
-    x[r] = acc / u[r][r];
-  }
-#pragma unroll
-  for (int q = 0; q < 5; ++q) x[q] *= sc[q];
-  return true;
+  for (int q = 0; q < 5; ++q) x[q] = xx[0][q];
+  return ok[0];
 }
 
 // lane -> (i, j) of the 15 unique A^T A entries; lanes 15..19 own A^T b[i].
@@ -296,6 +315,7 @@ __device__ bool update_linear(Ctx& c, int e) {
         nx.tauB *= gm;
         nx.tauS *= gm;
         g.lp = nx;
+        g.lp_ver += 1;
         g.cnt[3] += 1;
       }
     }
@@ -319,6 +339,7 @@ __device__ bool update_linear(Ctx& c, int e) {
   __syncwarp();
   if (c.lane == 0) {
     g.lp = nx;
+    g.lp_ver += 1;
     g.cnt[0] += 1;
     if (clamped) g.cnt[4] += 1;
   }
@@ -354,7 +375,8 @@ constexpr double kU = 1.1102230246251565e-16;  // 2^-53
 //   [5W,6W) 1/f_S per sample (only when s exceeds the token-count table)
 //   [6W, 6W+1024) 1/f_B by batch size   [6W+1024, 8W+1024) linear-tier rows
 //   [8W+1024, 9W+1024) distinct token counts (int32)
-//   [9W+1024, 9W+1024+kSTab) 1/f_S by token count
+//   [9W+1024, 10W+1024) 1/f_S by distinct-count index (dense)
+//   [10W+1024, 10W+1024+kSTab/2) token count -> dense index (int32)
 constexpr int kSTab = 10240;  // token-count table (bitmap fits the 1280 B stage)
 
 struct Stage {          // chronological window staged in the replica scratch
@@ -365,7 +387,8 @@ struct Stage {          // chronological window staged in the replica scratch
   double* ifs;          // 1 / f_S(s_i) for kS == ifs_k (when s exceeds the table)
   double* ifb;          // 1 / f_B(b) for kB == ifb_k, b in [1, tab]
   int* us;              // distinct s values of the window
-  double* stab;         // 1 / f_S(s) for s in us, kS == ifs_k
+  double* stab;         // 1 / f_S(us[k]) for kS == ifs_k, dense in k
+  int* s2id;            // s -> k with us[k] == s
   int n, tab, U;
   bool use_tab;
   double ifs_k, ifb_k;
@@ -384,6 +407,7 @@ __device__ __forceinline__ Stage stage_of(const Ctx& c) {
   s.ifb = c.scratch + 6 * W;
   s.us = reinterpret_cast<int*>(c.scratch + 8 * W + kFbTable);
   s.stab = c.scratch + 9 * W + kFbTable;
+  s.s2id = reinterpret_cast<int*>(c.scratch + 10 * W + kFbTable);
   s.n = 0;
   s.tab = 0;
   s.U = 0;
@@ -487,8 +511,10 @@ __device__ void stage_window(Ctx& c, const Window& w, const Params& cur, Stage& 
     sb[i] = b;
     ss[i] = s;
     sy[i] = y;
+    // {1/y, b | (distinct-s index << 16) | s << 32}; the index is filled in below
     rec[i] = make_double2(iy, __longlong_as_double(static_cast<long long>(
-                                  (static_cast<unsigned long long>(si) << 32) | static_cast<unsigned>(bi))));
+                                  (static_cast<unsigned long long>(si) << 32) |
+                                  static_cast<unsigned>(bi & 0xffff))));
     if (cur.kB * b < 20.0 || cur.kS * s < 20.0) unsat = true;
     if (si >= 64 && si >= 4 * bi) ++shp;
     bm = max(bm, bi);
@@ -508,7 +534,7 @@ __device__ void stage_window(Ctx& c, const Window& w, const Params& cur, Stage& 
   // distinct token counts: a presence bitmap in the shared stage, compacted
   // into S.us so each new kS costs one expm1 per distinct s, not per sample
   const int smax = warp_max_int(smx);
-  S.use_tab = smax < kSTab;
+  S.use_tab = smax < kSTab && bmax < 65536 && w.n <= 65536;
   if (S.use_tab) {
     uint32_t* bits = reinterpret_cast<uint32_t*>(c.chunk);
     const int words = (smax >> 5) + 1;
@@ -535,6 +561,15 @@ __device__ void stage_window(Ctx& c, const Window& w, const Params& cur, Stage& 
       base += __shfl_sync(NX_FULL, incl, 31);
     }
     S.U = base;
+    __syncwarp();
+    for (int k = c.lane; k < S.U; k += 32) S.s2id[S.us[k]] = k;
+    __syncwarp();
+    for (int i = c.lane; i < w.n; i += 32) {
+      const unsigned long long bits64 = static_cast<unsigned long long>(__double_as_longlong(rec[i].y));
+      const int si = static_cast<int>(bits64 >> 32);
+      rec[i].y = __longlong_as_double(static_cast<long long>(
+          bits64 | (static_cast<unsigned long long>(S.s2id[si]) << 16)));
+    }
   }
   __syncwarp();
 }
@@ -568,10 +603,8 @@ __device__ FitOut gauged_fit_impl(Ctx& c, Stage& S, const Params& cur, double kB
   if (new_s && S.use_tab) {
     __syncwarp();
 #pragma unroll 4
-    for (int k = c.lane; k < S.U; k += 32) {
-      const int sv = S.us[k];
-      S.stab[sv] = 1.0 / raw_factor(kS, static_cast<double>(sv));
-    }
+    for (int k = c.lane; k < S.U; k += 32)
+      S.stab[k] = 1.0 / raw_factor(kS, static_cast<double>(S.us[k]));
     __syncwarp();
   }
   const long long tf1 = nx_clock();
@@ -589,36 +622,41 @@ __device__ FitOut gauged_fit_impl(Ctx& c, Stage& S, const Params& cur, double kB
     t1 += u1; t2 += u2;
   };
   if (S.use_tab) {
-    // 4 samples per lane in flight: the record loads and the two table
+    // 8 samples per lane in flight: the record loads and the two table
     // gathers of a group issue back to back (memory-level parallelism)
+    auto unpack = [](double y, int& bi, int& id, int& si) {
+      const unsigned long long v = static_cast<unsigned long long>(__double_as_longlong(y));
+      bi = static_cast<int>(v & 0xffffull);
+      id = static_cast<int>((v >> 16) & 0xffffull);
+      si = static_cast<int>(v >> 32);
+    };
     int i = c.lane;
-    for (; i + 96 < n; i += 128) {
-      double2 r[4];
+    for (; i + 224 < n; i += 256) {
+      double2 r[8];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) r[u] = S.rec[i + 32 * u];
-      double fs[4];
-      int bi[4], si[4];
+      for (int u = 0; u < 8; ++u) r[u] = S.rec[i + 32 * u];
+      double fs[8];
+      int bi[8], si[8];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const long long bs = __double_as_longlong(r[u].y);
-        bi[u] = static_cast<int>(bs & 0xffffffffll);
-        si[u] = static_cast<int>(bs >> 32);
-        fs[u] = S.stab[si[u]];
+      for (int u = 0; u < 8; ++u) {
+        int id;
+        unpack(r[u].y, bi[u], id, si[u]);
+        fs[u] = S.stab[id];
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) accumulate(r[u].x, bi[u], si[u], fs[u]);
+      for (int u = 0; u < 8; ++u) accumulate(r[u].x, bi[u], si[u], fs[u]);
     }
     for (; i < n; i += 32) {
       const double2 r = S.rec[i];
-      const long long bs = __double_as_longlong(r.y);
-      const int bi = static_cast<int>(bs & 0xffffffffll), si = static_cast<int>(bs >> 32);
-      accumulate(r.x, bi, si, S.stab[si]);
+      int bi, id, si;
+      unpack(r.y, bi, id, si);
+      accumulate(r.x, bi, si, S.stab[id]);
     }
   } else {
     for (int i = c.lane; i < n; i += 32) {
       const double2 r = S.rec[i];
       const long long bs = __double_as_longlong(r.y);
-      const int bi = static_cast<int>(bs & 0xffffffffll), si = static_cast<int>(bs >> 32);
+      const int bi = static_cast<int>(S.sb[i]), si = static_cast<int>(bs >> 32);
       double ifs;
       if (new_s) {
         ifs = 1.0 / raw_factor(kS, static_cast<double>(si));
@@ -642,8 +680,16 @@ __device__ FitOut gauged_fit_impl(Ctx& c, Stage& S, const Params& cur, double kB
   FitOut out;
   out.err = __longlong_as_double(0x7ff0000000000000LL);
   out.bound = 0.0;
+  // unridged solve and the ridge at the cap (lambda = 1e-7, the value
+  // certified below in all but near-noise-free windows) run in lockstep
   double x[5];
-  if (!solve5_warp(e, x)) return out;
+  double vk[2] = {e, ridge_elem(e, 1e-7, prior)};
+  double xk[2][5];
+  bool okk[2];
+  solve5_warp_k<2>(vk, xk, okk);
+  if (!okk[0]) return out;
+#pragma unroll
+  for (int q = 0; q < 5; ++q) x[q] = xk[0][q];
   // lambda = min(1e-7, sse(x) / max(y2, 1e-30))  (learner.cpp:84-85, cap 1e-7)
   const double den = (y2 < 1e-30) ? 1e-30 : y2;
   // Certify sse(x) / den >= 1e-7 (=> lambda = cap) from a lower bound: the
@@ -676,7 +722,13 @@ __device__ FitOut gauged_fit_impl(Ctx& c, Stage& S, const Params& cur, double kB
     const double v = sse_x_exact(c, S, kB, kS, x) / den;
     lambda = (v < 1e-7) ? v : 1e-7;
   }
-  if (lambda > 1e-14 && !solve5_warp(ridge_elem(e, lambda, prior), x)) return out;
+  if (lambda == 1e-7) {
+    if (!okk[1]) return out;
+#pragma unroll
+    for (int q = 0; q < 5; ++q) x[q] = xk[1][q];
+  } else if (lambda > 1e-14 && !solve5_warp(ridge_elem(e, lambda, prior), x)) {
+    return out;
+  }
   const double tau0 = x[0] < 0.0 ? 0.0 : x[0];
   const double aa = x[1] < 0.0 ? 0.0 : x[1];
   const double slope = cur.ws / cur.p_max + cur.tauS;
@@ -808,6 +860,7 @@ __device__ void update_structural(Ctx& c, int e) {
   __syncwarp();
   if (c.lane == 0) {
     g.lp = best.p;
+    g.lp_ver += 1;
     g.cnt[1] += 1;
   }
   __syncwarp();

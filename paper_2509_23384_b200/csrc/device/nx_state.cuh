@@ -36,6 +36,10 @@ struct EngSm {
   int32_t ring_size, ring_head, tw_head, tw_len, dq_head, dq_len, lat_head, lat_len;
   int32_t has_rep, noise_pos;
   int32_t refit_pending;                       // structural refit queued / running
+  // decode-only step memo: T(R, R) under the learner params (valid while
+  // lp_ver is unchanged) and under the ground truth
+  int32_t lp_ver, memo_ver, memo_b, memo_tb;
+  double memo_pred, memo_truth;
 };
 
 struct RepSm {

@@ -346,17 +346,43 @@ __device__ void try_begin_step(Ctx& c, int e, int64_t now_us) {
   wait_refit(c, e);  // planning reads the learner's params
   PhaseTimer pt(c.rs, 2);
   const NxEngineDesc& ed = c.ed[e];
-  if (ed.policy == 0) plan_lens(c, e);
-  else plan_baseline(c, e);
-  if (failed(c) || g.plan_n == 0) return;
-  trim_for_kv(c, e);
-  if (g.plan_n == 0) return;
   const bool noisy = ed.noise_sigma != 0.0;
+  const int R = g.rq_len;
+  double truth;
+  if (ed.policy == 0 && g.wq_len == 0 && R <= ed.q_max) {
+    // Decode-only LENS step: with an empty wait queue the sweep has the single
+    // candidate B = R, S = R (lens.cpp:121-146), and there is no prefill for
+    // trim_for_kv to admit. The scheduler's and the oracle's predictions of
+    // the same shape are independent chains, evaluated together.
+    // Both values are memoised per engine: at low load R repeats for many
+    // consecutive steps (same inputs, same value).
+    const double bd = static_cast<double>(R);
+    const bool hit_p = g.memo_b == R && g.memo_ver == g.lp_ver;
+    const bool hit_t = g.memo_tb == R;
+    const double pred = hit_p ? g.memo_pred : predict(g.lp, bd, bd);
+    truth = hit_t ? g.memo_truth : predict(params_from(ed.tp), bd, bd);
+    __syncwarp();
+    if (c.lane == 0) {
+      g.memo_b = R;
+      g.memo_ver = g.lp_ver;
+      g.memo_pred = pred;
+      g.memo_tb = R;
+      g.memo_truth = truth;
+    }
+    write_decodes(c, c.P->rq + ed.rq_off, R, c.P->plan_req + ed.plan_off, c.P->plan_tok + ed.plan_off);
+    set_plan(c, g, R, R, R, pred, 0.0, 0, 0, R);
+  } else {
+    if (ed.policy == 0) plan_lens(c, e);
+    else plan_baseline(c, e);
+    if (failed(c) || g.plan_n == 0) return;
+    if (g.plan_ndec < g.plan_n) trim_for_kv(c, e);
+    if (g.plan_n == 0) return;
+    truth = predict(params_from(ed.tp), g.plan_b, g.plan_s);  // oracle_latency (engine.cpp:128-132)
+  }
   if (noisy && g.noise_pos >= 32) refill_noise(c, e);
   __syncwarp();
   if (c.lane == 0) {
-    const Params tp = params_from(ed.tp);
-    double actual = predict(tp, g.plan_b, g.plan_s);  // oracle_latency (engine.cpp:128-132)
+    double actual = truth;
     if (noisy) actual = actual * g.noise[g.noise_pos++];
     const int64_t d = to_us(actual);
     g.busy = 1;
@@ -939,6 +965,7 @@ __device__ void init_replica(Ctx& c) {
     g.ring_size = 0; g.ring_head = 0; g.tw_head = 0; g.tw_len = 0;
     g.dq_head = 0; g.dq_len = 0; g.lat_head = 0; g.lat_len = 0; g.has_rep = 0;
     g.dq_t0 = kNoEvent; g.dq_s0 = 0; g.noise_pos = 32; g.refit_pending = 0;
+    g.lp_ver = 0; g.memo_ver = -1; g.memo_b = -1; g.memo_tb = -1; g.memo_pred = 0.0; g.memo_truth = 0.0;
   }
   if (c.lane == 0) {
     RepSm& R = *c.rs;
@@ -1066,9 +1093,32 @@ __device__ void run_replica(Ctx& c) {
         if (ok) try_begin_step(c, e, now);
         break;
       }
-      case 1:
+      case 1: {
         step_complete(c, who, now);
+        // The learner update just queued at (now, seq) is the next event
+        // unless another pending event shares this timestamp (all of those
+        // carry smaller sequence numbers): then process it right here.
+        if (failed(c)) break;
+        bool other = false;
+        if (c.lane < c.n_eng) {
+          const EngSm& g = c.eng[c.lane];
+          other = g.step_t == now_u || g.report_t == now_u || g.dq_t0 == now_u ||
+                  (c.lane != who && g.learn_t == now_u);
+        }
+        if (c.lane == 0 && c.rs->next_arr == now_u) other = true;
+        if (__any_sync(NX_FULL, other)) break;
+        __syncwarp();
+        if (c.lane == 0) {
+          c.eng[who].learn_t = kNoEvent;
+          c.rs->ev_hash = fnv_event(c.rs->ev_hash, now_u, 3ull,
+                                    static_cast<uint64_t>(c.ed[who].engine_id + 1), 0ull);
+          c.rs->events += 1;
+        }
+        __syncwarp();
+        const EngSm& g = c.eng[who];
+        record_sample(c, who, g.learn_b, g.learn_s, g.learn_y);
         break;
+      }
       case 2: {
         PhaseTimer pt(c.rs, 4);
         state_report(c, who, now);

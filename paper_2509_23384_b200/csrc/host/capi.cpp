@@ -196,7 +196,7 @@ void fill_descriptors(nx_sim& h) {
     d.min_s = static_cast<int32_t>(std::min<int64_t>(c.min_structural, INT32_MAX));
     req_off += n;
     sess_off += ns;
-    scratch_off += (9 * static_cast<int64_t>(c.long_window) + 1024 + 10240 + 64 + 31) / 32 * 32;  // nx_learner.cuh layout
+    scratch_off += (10 * static_cast<int64_t>(c.long_window) + 1024 + 5120 + 64 + 31) / 32 * 32;  // nx_learner.cuh layout
     for (const auto& ec : c.engines) {
       NxEngineDesc e;
       std::memset(&e, 0, sizeof e);

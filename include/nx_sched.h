@@ -28,6 +28,11 @@ enum { NX_OK = 0, NX_EINVAL = 1, NX_ERUNTIME = 2, NX_ELOGIC = 3, NX_ECUDA = 4 };
 enum { NX_DETERMINISTIC_FP64 = 0, NX_FAST_FP32 = 1 };
 
 const char* nx_last_error(void);
+/* sizeof of the ABI structs, in declaration order (nx_lens_problem,
+ * nx_lens_plan, nx_route_group, nx_engine_report, nx_route_request,
+ * nx_route_decision, nx_refit_problem, nx_refit_result, nx_replica_summary,
+ * nx_request_record) — lets bindings verify their layouts. */
+int nx_abi_sizes(int64_t* out, int32_t n);
 int nx_device_count(void);
 
 /* ---- K1: batched perf-model evaluation ------------------------------------
@@ -54,6 +59,139 @@ int nx_perf_eval_async(const double* params, int32_t n_params, const int32_t* id
 int nx_perf_eval_host(const double* params, int32_t n_params, const int32_t* idx,
                       const int32_t* b, const int32_t* s, double* out_T, double* out_thr,
                       int64_t n, int32_t mode);
+
+/* ---- K2: batched LENS scheduling decisions --------------------------------
+ * Replaces servesim::schedule_step (proj/include/servesim/lens.h:114-124,
+ * proj/src/lens.cpp:96-146): one independent decision per problem — the
+ * candidate batch-size sweep, binary_search_budget per candidate
+ * (lens.cpp:33-56), allocate_tokens/realize (:58-92) and the first-min /
+ * early-exit selection. Run-queue requests need no per-request data (each
+ * takes one decode token); waiters are given by their remaining prompt.
+ * Status per problem mirrors the reference's exceptions: NX_EINVAL for an
+ * invalid SchedulerConfig, SLOSpec, TradeoffModel or PerfParams, a
+ * non-positive target, or (device limit) remaining < 1 / q_max, m_max >= 2^30. */
+typedef struct nx_lens_problem {
+  double params[8];                   /* PerfParams {tau0,w0,ws,tauB,tauS,p_max,kB,kS} */
+  double ttft_slo_ms, tpot_slo_ms;    /* SLOSpec (lens.h:14-19) */
+  double alpha_ms, beta, l_bar, td_min_ms; /* TradeoffModel (lens.h:22-38) */
+  double eps_ratio, q_ref;            /* SchedulerConfig (lens.h:63-75) */
+  int64_t m_max, q_max;
+  int32_t n_search_iters;
+  int32_t n_run;                      /* |run_q| */
+  int32_t n_wait;                     /* |wait_q| (FCFS order) */
+  int32_t pad_;
+  int64_t wait_off;                   /* waiters at [wait_off, wait_off + n_wait) */
+} nx_lens_problem;
+
+typedef struct nx_lens_plan {         /* BatchPlan (lens.h:82-91) */
+  int64_t b, s;
+  double predicted_ms, target_ms;
+  int32_t overload;                   /* run queue exceeded q_max: truncated decode plan */
+  int32_t slo_risk;                   /* TargetLatency::slo_risk */
+  int32_t n_decode;                   /* allocations [0, n_decode): run_q[i], 1 token */
+  int32_t n_prefill;                  /* then wait_q[k], k < n_prefill, alloc_tokens[wait_off+k] tokens */
+  int32_t status;                     /* NX_OK / NX_EINVAL */
+  int32_t pad_;
+} nx_lens_plan;
+
+/* Device pointers, stream-ordered. wait_remaining: prompt_len - prefilled per
+ * waiter (int32, >= 1). alloc_tokens: written for admitted waiters only. */
+int nx_lens_schedule_dev(const nx_lens_problem* problems, int32_t n_problems,
+                         const int32_t* wait_remaining, int64_t n_wait_total,
+                         nx_lens_plan* plans, int32_t* alloc_tokens, void* stream);
+/* Host pointers: copies in/out inside the call; returns the first failing
+ * problem's status (all plans are still written). */
+int nx_lens_schedule_host(const nx_lens_problem* problems, int32_t n_problems,
+                          const int32_t* wait_remaining, int64_t n_wait_total,
+                          nx_lens_plan* plans, int32_t* alloc_tokens);
+
+/* ---- K3: batched PRISM routing ---------------------------------------------
+ * Replaces servesim::Router::route (proj/include/servesim/router.h:55-121,
+ * proj/src/router.cpp:141-289). A group is one Router: its engines (in
+ * registration order, <= 32), report table, session map, RNG and
+ * round-robin cursor; its requests are routed in order, each decision
+ * seeing the previous ones' dispatch echo (router.cpp:275-282) and session
+ * memory (remember_session). Groups are independent (one warp each).
+ * Policies: 0 prism, 1 round_robin, 2 session_affinity, 3 least_loaded,
+ * 5 weighted (4 latency_based needs completion history: NX_EINVAL).
+ * Report rows and group state (l_bar_ema, rng, rr_next, session map) are
+ * updated in place, as the Router's own state would be. */
+typedef struct nx_route_group {
+  double weights[4];                  /* RouterConfig (router.h:31-52) */
+  double beta_aff, latency_knee, latency_scale_ms, load_half_ms, capacity_headroom,
+      staleness_limit_ms;
+  double ttft_slo_ms;                 /* SLOSpec::ttft_slo_ms */
+  double l_bar_ema;                   /* router-side decode-length estimate (router.h:118) */
+  uint64_t rng[4];                    /* weighted-policy xoshiro256++ state */
+  uint64_t rr_next;                   /* round-robin cursor */
+  int32_t policy, n_engines;
+  int64_t engine_off;                 /* report rows [engine_off, +n_engines) */
+  int64_t request_off;                /* requests [request_off, +n_requests) */
+  int64_t session_off;                /* session map [session_off, +n_sessions) */
+  int32_t n_requests, n_sessions;     /* n_sessions <= 100000 (router.h:107) */
+} nx_route_group;
+
+typedef struct nx_engine_report {     /* EngineReport (engine.h:50-67) + registration */
+  double l_hat_ms, w_load_tokens, m_free_tokens, p_max, reported_at_ms;
+  double static_weight;               /* RouterConfig::static_weights[engine_id] (1.0 if unset) */
+  int64_t queue_len;
+  int32_t engine_id;
+  int32_t has_report;                 /* 0: no report received yet */
+} nx_engine_report;
+
+typedef struct nx_route_request {
+  double now_ms;
+  int64_t prompt_len;
+  int32_t session;                    /* index into the group's session map */
+  int32_t pad_;
+} nx_route_request;
+
+typedef struct nx_route_decision {    /* RouteDecision (router.h:67-72) */
+  double score, factors[4];
+  int32_t engine_id;
+  int32_t degraded;
+} nx_route_decision;
+
+/* session_map: per group, engine index last routed for each session or -1. */
+int nx_prism_route_dev(nx_route_group* groups, int32_t n_groups, nx_engine_report* reports,
+                       const nx_route_request* requests, int32_t* session_map,
+                       nx_route_decision* decisions, int32_t* group_status, void* stream);
+int nx_prism_route_host(nx_route_group* groups, int32_t n_groups, nx_engine_report* reports,
+                        int64_t n_reports, const nx_route_request* requests, int64_t n_requests,
+                        int32_t* session_map, int64_t n_session_entries,
+                        nx_route_decision* decisions, int32_t* group_status);
+
+/* ---- K4: batched learner refits ---------------------------------------------
+ * Replaces OnlineLearner::update_linear / update_structural
+ * (proj/include/servesim/learner.h:70-80, proj/src/learner.cpp:300-440) on
+ * explicit windows: each problem is one learner whose ring holds
+ * samples [sample_off, sample_off + n_samples) in chronological order (the
+ * last long_window of them are the window). One warp per problem. */
+typedef struct nx_refit_problem {
+  double params[8];                   /* OnlineLearner::params() before the update */
+  int64_t long_window, short_window, min_structural_samples;
+  int64_t sample_off;
+  int32_t n_samples;
+  int32_t pad_;
+} nx_refit_problem;
+
+typedef struct nx_refit_result {
+  double params[8];                   /* params() after the update */
+  int64_t counters[7];                /* LearnerCounters increments (learner.h:26-34) */
+  int32_t updated;                    /* the update's return value */
+  int32_t status;                     /* NX_OK / NX_EINVAL (invalid sample / config) */
+} nx_refit_result;
+
+enum { NX_REFIT_LINEAR = 0, NX_REFIT_STRUCTURAL = 1 };
+
+/* max_long_window: upper bound of problems[i].long_window (sizes the per-warp
+ * scratch; a problem above it gets NX_EINVAL). */
+int nx_refit_dev(int32_t kind, const nx_refit_problem* problems, int32_t n_problems,
+                 const int32_t* sample_b, const int32_t* sample_s, const double* sample_y,
+                 int64_t max_long_window, nx_refit_result* results, void* stream);
+int nx_refit_host(int32_t kind, const nx_refit_problem* problems, int32_t n_problems,
+                  const int32_t* sample_b, const int32_t* sample_s, const double* sample_y,
+                  int64_t n_samples_total, nx_refit_result* results);
 
 /* ---- K5 (+K2/K3/K4 inside): batched replica simulation --------------------
  * Replaces servesim::run_simulation / sweep (proj/include/servesim/sim.h:
@@ -111,6 +249,9 @@ int nx_sim_work(nx_sim_t h, int32_t replica, int64_t* out6);
  * warp, overlapped with the event loop), [7] deliveries, [8] event loop
  * blocked on a pending refit, [9]-[15] refit internals (diagnostic) */
 int nx_sim_phase_cycles(nx_sim_t h, int32_t replica, int64_t* out10);
+/* %globaltimer (ns) at which the replica's CTA started and finished it
+ * (diagnostic: per-replica latency under co-residency). */
+int nx_sim_timeline(nx_sim_t h, int32_t replica, int64_t* begin_end_ns);
 /* Learner state per engine: params[8] + samples + counters[7]. */
 int nx_sim_learner(nx_sim_t h, int32_t replica, int32_t engine, double* params8,
                    int64_t* samples, int64_t* counters7);

@@ -380,4 +380,134 @@ int ref_learner_structural(const double* priors8, int64_t window,
   }
 }
 
+// Router over a sequence: registers engines (ids in order, static weights),
+// replays completions (engine id, session "s<k>", decode length) through
+// on_completion, installs reports, then routes the requests in order.
+// Returns every RouteDecision and the final report view (dispatch echoes).
+int ref_route_group(int policy, const double* router_cfg9, double ttft, double tpot,
+                    uint64_t root_seed, int n_engines, const int* engine_ids,
+                    const double* static_w, const double* states5, const int64_t* queue_len,
+                    const int* has_report, int n_comp, const int* comp_engine,
+                    const int* comp_session, const int64_t* comp_decode, int n_req,
+                    const int64_t* req_prompt, const int* req_session, const double* req_now,
+                    int* out_engine, double* out_score, double* out_factors, int* out_degraded,
+                    double* out_states5, int64_t* out_qlen) {
+  try {
+    RouterConfig cfg;
+    cfg.policy = static_cast<RouterPolicy>(policy);
+    for (int i = 0; i < 4; ++i) cfg.weights[i] = router_cfg9[i];
+    cfg.beta_aff = router_cfg9[4];
+    cfg.latency_knee = router_cfg9[5];
+    cfg.latency_scale_ms = router_cfg9[6];
+    cfg.load_half_ms = router_cfg9[7];
+    cfg.capacity_headroom = router_cfg9[8];
+    for (int e = 0; e < n_engines; ++e)
+      if (static_w[e] != 1.0) cfg.static_weights[engine_ids[e]] = static_w[e];
+    Router router(cfg, {ttft, tpot}, root_seed);
+    for (int e = 0; e < n_engines; ++e) router.register_engine(engine_ids[e]);
+    for (int k = 0; k < n_comp; ++k)
+      router.on_completion(comp_engine[k], "s" + std::to_string(comp_session[k]), 1.0,
+                           comp_decode[k], 0.0);
+    std::vector<EngineReport> view(n_engines);
+    for (int e = 0; e < n_engines; ++e) {
+      if (!has_report[e]) continue;
+      EngineReport rep;
+      rep.state.engine_id = engine_ids[e];
+      rep.state.l_hat_ms = states5[5 * e + 0];
+      rep.state.w_load_tokens = states5[5 * e + 1];
+      rep.state.m_free_tokens = states5[5 * e + 2];
+      rep.state.p_max = states5[5 * e + 3];
+      rep.state.reported_at_ms = states5[5 * e + 4];
+      rep.queue_len = queue_len[e];
+      router.on_report(rep);
+      view[e] = rep;
+    }
+    for (int k = 0; k < n_req; ++k) {
+      Request req;
+      req.id = static_cast<uint64_t>(k);
+      req.session_id = "s" + std::to_string(req_session[k]);
+      req.prompt_len = req_prompt[k];
+      const RouteDecision d = router.route(req, req_now[k]);
+      out_engine[k] = d.engine_id;
+      out_score[k] = d.score;
+      for (int i = 0; i < 4; ++i) out_factors[4 * k + i] = d.factors[i];
+      out_degraded[k] = d.degraded;
+      // mirror the dispatch echo into the returned view (router.cpp:275-282)
+      if (cfg.policy == RouterPolicy::kPrism) {
+        for (int e = 0; e < n_engines; ++e)
+          if (engine_ids[e] == d.engine_id && has_report[e]) {
+            view[e].queue_len += 1;
+            view[e].state.w_load_tokens += static_cast<double>(req.prompt_len) + 32.0;
+          }
+      }
+    }
+    for (int e = 0; e < n_engines; ++e) {
+      out_states5[5 * e + 0] = view[e].state.l_hat_ms;
+      out_states5[5 * e + 1] = view[e].state.w_load_tokens;
+      out_states5[5 * e + 2] = view[e].state.m_free_tokens;
+      out_states5[5 * e + 3] = view[e].state.p_max;
+      out_states5[5 * e + 4] = view[e].state.reported_at_ms;
+      out_qlen[e] = view[e].queue_len;
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return classify(e);
+  }
+}
+
+// Single linear update on a prepared window (same ring set-up as
+// ref_learner_structural, then update_linear()).
+int ref_learner_linear(const double* priors8, int64_t window, int64_t short_window,
+                       const int64_t* b, const int64_t* s, const double* y, int64_t n,
+                       double* out_params8, int* accepted, int64_t* out_counters7) {
+  try {
+    LearnerConfig cfg;
+    cfg.long_window = window;
+    cfg.short_window = short_window;
+    cfg.structural_period = 1 << 30;
+    cfg.linear_period = (1 << 30) - 1;
+    cfg.min_structural_samples = 1;
+    OnlineLearner learner(params_from(priors8), cfg);
+    for (int64_t i = 0; i < n; ++i) learner.record_sample({{b[i], s[i]}, y[i], 0.0});
+    *accepted = learner.update_linear();
+    params_to(learner.params(), out_params8);
+    const auto& c = learner.counters();
+    const int64_t cv[7] = {c.linear_updates, c.structural_updates, c.degenerate_updates,
+                           c.rescale_updates, c.clamp_events, c.failed_fits, c.low_identifiability};
+    for (int i = 0; i < 7; ++i) out_counters7[i] = cv[i];
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return classify(e);
+  }
+}
+
+// Structural update with explicit short window / min samples; counters out.
+int ref_learner_structural2(const double* priors8, int64_t window, int64_t short_window,
+                            int64_t min_samples, const int64_t* b, const int64_t* s,
+                            const double* y, int64_t n, double* out_params8, int* accepted,
+                            int64_t* out_counters7) {
+  try {
+    LearnerConfig cfg;
+    cfg.long_window = window;
+    cfg.short_window = short_window;
+    cfg.structural_period = 1 << 30;
+    cfg.linear_period = (1 << 30) - 1;
+    cfg.min_structural_samples = min_samples;
+    OnlineLearner learner(params_from(priors8), cfg);
+    for (int64_t i = 0; i < n; ++i) learner.record_sample({{b[i], s[i]}, y[i], 0.0});
+    *accepted = learner.update_structural();
+    params_to(learner.params(), out_params8);
+    const auto& c = learner.counters();
+    const int64_t cv[7] = {c.linear_updates, c.structural_updates, c.degenerate_updates,
+                           c.rescale_updates, c.clamp_events, c.failed_fits, c.low_identifiability};
+    for (int i = 0; i < 7; ++i) out_counters7[i] = cv[i];
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return classify(e);
+  }
+}
+
 }  // extern "C"

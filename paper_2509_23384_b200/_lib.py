@@ -7,9 +7,10 @@ CUDA device is visible, calls raise.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
-SO_PATH = Path(__file__).resolve().parent / "_nxsched.so"
+SO_PATH = Path(__file__).resolve().parent / os.environ.get("NX_SO", "_nxsched.so")
 
 NX_OK, NX_EINVAL, NX_ERUNTIME, NX_ELOGIC, NX_ECUDA = 0, 1, 2, 3, 4
 NX_DETERMINISTIC_FP64, NX_FAST_FP32 = 0, 1
@@ -66,6 +67,7 @@ def lib() -> C.CDLL:
     L.nx_sim_destroy.restype = None
     L.nx_sim_work.argtypes = [C.c_void_p, C.c_int32, _P(C.c_int64)]
     L.nx_sim_phase_cycles.argtypes = [C.c_void_p, C.c_int32, _P(C.c_int64)]
+    L.nx_sim_timeline.argtypes = [C.c_void_p, C.c_int32, _P(C.c_int64)]
     L.nx_sim_copy_summaries.argtypes = [C.c_void_p, C.c_void_p]
     L.nx_sim_summaries_dev.argtypes = [C.c_void_p, _P(C.c_void_p), _P(C.c_int64)]
     L.nx_perf_eval_dev.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
@@ -78,6 +80,14 @@ def lib() -> C.CDLL:
     L.nx_workload_info.argtypes = [C.c_char_p, _P(C.c_uint64), _P(C.c_int64), _P(C.c_int64)]
     L.nx_synth_generate.argtypes = [C.c_char_p, C.c_int64, C.c_uint64, _P(C.c_int64),
                                     _P(C.c_int64), C.c_char_p]
+    V = C.c_void_p
+    L.nx_abi_sizes.argtypes = [_P(C.c_int64), C.c_int32]
+    L.nx_lens_schedule_dev.argtypes = [V, C.c_int32, V, C.c_int64, V, V, V]
+    L.nx_lens_schedule_host.argtypes = [V, C.c_int32, V, C.c_int64, V, V]
+    L.nx_prism_route_dev.argtypes = [V, C.c_int32, V, V, V, V, V, V]
+    L.nx_prism_route_host.argtypes = [V, C.c_int32, V, C.c_int64, V, C.c_int64, V, C.c_int64, V, V]
+    L.nx_refit_dev.argtypes = [C.c_int32, V, C.c_int32, V, V, V, C.c_int64, V, V]
+    L.nx_refit_host.argtypes = [C.c_int32, V, C.c_int32, V, V, V, C.c_int64, V]
     _lib = L
     return L
 

@@ -34,8 +34,14 @@ __device__ __forceinline__ double pick5(const double v[5], int k) {
 
 // K independent systems in lockstep: their shuffle and division latencies
 // overlap. ok[k] reports each system's rank test separately.
+// Out of line and with the column loop rolled: one ~1k-instruction copy per K
+// instead of a ~4k-instruction straight-line body inlined at every call site.
+// It runs once per structural fit on the refit warp, and its unrolled body
+// streamed through the SM's instruction cache evicted the co-resident event
+// loops' hot code (ncu: no_instruction stalls 1.0 -> 6.6 cycles/issue at 3.5
+// replica CTAs per SM).
 template <int K>
-__device__ void solve5_warp_k(double (&v)[K], double (&x)[K][5], bool (&ok)[K]) {
+static __device__ __noinline__ void solve5_warp_k(double (&v)[K], double (&x)[K][5], bool (&ok)[K]) {
   const int lane = lane_id();
   const bool isA = lane < 25;
   const int i = isA ? lane / 5 : (lane < 30 ? lane - 25 : 0);
@@ -57,7 +63,7 @@ __device__ void solve5_warp_k(double (&v)[K], double (&x)[K][5], bool (&ok)[K]) 
     for (int o = 16; o > 0; o >>= 1) nm = dmax(nm, __shfl_xor_sync(NX_FULL, nm, o));
     norm[k] = nm;
   }
-#pragma unroll
+#pragma unroll 1
   for (int col = 0; col < 5; ++col) {
 #pragma unroll
     for (int k = 0; k < K; ++k) {
@@ -65,10 +71,13 @@ __device__ void solve5_warp_k(double (&v)[K], double (&x)[K][5], bool (&ok)[K]) 
 #pragma unroll
       for (int r = 0; r < 5; ++r) cv[r] = fabs(__shfl_sync(NX_FULL, v[k], r * 5 + col));
       int piv = col;
-      double pv = cv[col];
+      double pv = 0.0;
 #pragma unroll
-      for (int r = col + 1; r < 5; ++r)
-        if (cv[r] > pv) {
+      for (int r = 0; r < 5; ++r)
+        if (r == col) pv = cv[r];
+#pragma unroll
+      for (int r = 1; r < 5; ++r)  // first strict maximum below the diagonal
+        if (r > col && cv[r] > pv) {
           piv = r;
           pv = cv[r];
         }
@@ -216,7 +225,7 @@ __device__ __forceinline__ Window window_of(const Ctx& c, int e, int n_want) {
 }
 
 // ---- linear tier (learner.cpp:160-207, 300-344) ------------------------------
-__device__ bool update_linear(Ctx& c, int e) {
+static __device__ NX_COLD bool update_linear(Ctx& c, int e) {
   EngSm& g = c.eng[e];
   const Window w = window_of(c, e, c.d->short_w);
   const int n = w.n;
@@ -418,7 +427,7 @@ __device__ __forceinline__ Stage stage_of(const Ctx& c) {
 }
 
 // windowed_sse (learner.cpp:209-222), direct model evaluation, tree order
-__device__ double wsse_tree(Ctx& c, const Stage& S, const Params& p) {
+static __device__ NX_COLD double wsse_tree(Ctx& c, const Stage& S, const Params& p) {
   double part = 0.0;
   for (int i = c.lane; i < S.n; i += 32) {
     const double y = S.sy[i];
@@ -428,7 +437,7 @@ __device__ double wsse_tree(Ctx& c, const Stage& S, const Params& p) {
   return warp_sum(part);
 }
 // the same sum in the reference's left-to-right order
-__device__ double wsse_exact(Ctx& c, const Stage& S, const Params& p) {
+static __device__ NX_COLD double wsse_exact(Ctx& c, const Stage& S, const Params& p) {
   double run = 0.0;
   for (int base = 0; base < S.n; base += 32) {
     const int i = base + c.lane;
@@ -444,7 +453,7 @@ __device__ double wsse_exact(Ctx& c, const Stage& S, const Params& p) {
 }
 // gauged_fit's ridge-scale sse(x) exactly as the reference forms it
 // (rows (1, 1/f, s/f, b, s), f = max(fB fS, 1e-300); learner.cpp:234-260)
-__device__ double sse_x_exact(Ctx& c, const Stage& S, double kB, double kS, const double x[5]) {
+static __device__ NX_COLD double sse_x_exact(Ctx& c, const Stage& S, double kB, double kS, const double x[5]) {
   double run = 0.0;
   for (int base = 0; base < S.n; base += 32) {
     const int i = base + c.lane;
@@ -471,7 +480,7 @@ __device__ double sse_x_exact(Ctx& c, const Stage& S, double kB, double kS, cons
 // SSE(x) = y2 - 2 x.t + x^T A x with its absolute rounding bound: accumulation
 // error of every entry (all terms positive) plus the closed-form arithmetic,
 // plus the per-term gap between x.row and the reference's model evaluation.
-__device__ void closed_sse(double e, const double x[5], int n, double y2, double& val,
+static __device__ NX_COLD void closed_sse(double e, const double x[5], int n, double y2, double& val,
                            double& bound) {
   const int lane = lane_id();
   double q = 0.0, qa = 0.0, l = 0.0, la = 0.0;
@@ -493,7 +502,7 @@ __device__ void closed_sse(double e, const double x[5], int n, double y2, double
 }
 
 // Per-update staging: chronological copy, gate statistics, invariant sums.
-__device__ void stage_window(Ctx& c, const Window& w, const Params& cur, Stage& S, bool& saturated,
+static __device__ NX_COLD void stage_window(Ctx& c, const Window& w, const Params& cur, Stage& S, bool& saturated,
                              int& shaped, int& bmax) {
   double* sb = const_cast<double*>(S.sb);
   double* ss = const_cast<double*>(S.ss);
@@ -580,14 +589,14 @@ struct FitOut {
 };
 
 // gauged_fit (learner.cpp:228-298) for fixed (kB, kS).
-__device__ FitOut gauged_fit_impl(Ctx& c, Stage& S, const Params& cur, double kB, double kS);
-__device__ FitOut gauged_fit(Ctx& c, Stage& S, const Params& cur, double kB, double kS) {
+static __device__ FitOut gauged_fit_impl(Ctx& c, Stage& S, const Params& cur, double kB, double kS);
+static __device__ FitOut gauged_fit(Ctx& c, Stage& S, const Params& cur, double kB, double kS) {
   const long long t0 = nx_clock();
   FitOut o = gauged_fit_impl(c, S, cur, kB, kS);
   if (c.lane == 0) count(c.rs->cycles[10], nx_clock() - t0);
   return o;
 }
-__device__ FitOut gauged_fit_impl(Ctx& c, Stage& S, const Params& cur, double kB, double kS) {
+static __device__ NX_COLD FitOut gauged_fit_impl(Ctx& c, Stage& S, const Params& cur, double kB, double kS) {
   if (c.lane == 0) count(c.rs->work[5], 1);
   const int n = S.n;
   const long long tf0 = nx_clock();
@@ -756,14 +765,14 @@ __device__ FitOut gauged_fit_impl(Ctx& c, Stage& S, const Params& cur, double kB
 
 // Certified "exact(a) < exact(b) * f" for two windowed-SSE intervals; exact
 // re-evaluation only when the intervals cannot decide.
-__device__ bool less_scaled_impl(Ctx& c, const Stage& S, const FitOut& a, const FitOut& b, double f);
-__device__ bool less_scaled(Ctx& c, const Stage& S, const FitOut& a, const FitOut& b, double f) {
+static __device__ bool less_scaled_impl(Ctx& c, const Stage& S, const FitOut& a, const FitOut& b, double f);
+static __device__ bool less_scaled(Ctx& c, const Stage& S, const FitOut& a, const FitOut& b, double f) {
   const long long t0 = nx_clock();
   const bool r = less_scaled_impl(c, S, a, b, f);
   if (c.lane == 0) count(c.rs->cycles[11], nx_clock() - t0);
   return r;
 }
-__device__ bool less_scaled_impl(Ctx& c, const Stage& S, const FitOut& a, const FitOut& b, double f) {
+static __device__ NX_COLD bool less_scaled_impl(Ctx& c, const Stage& S, const FitOut& a, const FitOut& b, double f) {
   const double a_hi = a.err + a.bound, a_lo = a.err - a.bound;
   const double b_hi = (b.err + b.bound) * f, b_lo = (b.err - b.bound) * f;
   if (a_hi < b_lo * (1.0 - 4.0 * kU)) return true;
@@ -771,7 +780,7 @@ __device__ bool less_scaled_impl(Ctx& c, const Stage& S, const FitOut& a, const 
   return wsse_exact(c, S, a.p) < wsse_exact(c, S, b.p) * f;
 }
 
-__device__ void update_structural(Ctx& c, int e) {
+static __device__ NX_COLD void update_structural(Ctx& c, int e) {
   EngSm& g = c.eng[e];
   const Window w = window_of(c, e, c.d->long_w);
   const int n = w.n;
@@ -870,7 +879,7 @@ __device__ void update_structural(Ctx& c, int e) {
 // Queue a structural refit of engine e for the refit warp. The engine's
 // learner state (params, ring, counters) is frozen until the refit clears
 // refit_pending: the event loop waits (wait_refit) before its next read.
-__device__ void post_refit(Ctx& c, int e) {
+static __device__ void post_refit(Ctx& c, int e) {
   __syncwarp();
   if (c.lane == 0) {
     vstore(c.eng[e].refit_pending, 1);
@@ -883,7 +892,7 @@ __device__ void post_refit(Ctx& c, int e) {
 }
 
 // Tells the refit warp the replica is done (job id -1).
-__device__ void post_exit(Ctx& c) {
+static __device__ void post_exit(Ctx& c) {
   __syncwarp();
   if (c.lane == 0) {
     const int t = vload(c.rs->jq_tail);
@@ -894,7 +903,7 @@ __device__ void post_exit(Ctx& c) {
   __syncwarp();
 }
 
-__device__ void wait_refit(Ctx& c, int e) {
+static __device__ void wait_refit(Ctx& c, int e) {
   if (!vload(c.eng[e].refit_pending)) return;
   const long long t0 = nx_clock();
   while (vload(c.eng[e].refit_pending)) __nanosleep(64);
@@ -904,7 +913,7 @@ __device__ void wait_refit(Ctx& c, int e) {
 }
 
 // The refit warp: pops engine ids and runs update_structural until it pops -1.
-__device__ void refit_worker(Ctx& c) {
+static __device__ NX_COLD void refit_worker(Ctx& c) {
   while (true) {
     int e = -2;
     if (c.lane == 0) {
@@ -934,7 +943,7 @@ __device__ void refit_worker(Ctx& c) {
 }
 
 // record_sample (learner.cpp:130-146): ring push + periodic refits.
-__device__ void record_sample(Ctx& c, int e, int b, int s, double y) {
+static __device__ NX_COLD void record_sample(Ctx& c, int e, int b, int s, double y) {
   EngSm& g = c.eng[e];
   wait_refit(c, e);
   if (!(y > 0.0) || !(b >= 1 && s >= b)) {

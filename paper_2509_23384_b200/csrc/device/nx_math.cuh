@@ -33,7 +33,23 @@ __device__ __forceinline__ bool params_valid(const Params& p) {  // perf_model.c
 // (perf_model.cpp:12-20).
 constexpr double kFactorMax = 0x1.fffffffffffffp-1;
 
-__device__ __forceinline__ double raw_factor(double k, double x) { return -expm1(-k * x); }
+// -expm1(-kx) for kx >= 45: e^-45 < 2^-64, so the exact value 1 - e^-kx
+// rounds to 1.0 in double (any expm1 within 1 ulp returns -1 there); the
+// transcendental is skipped. Most LENS probes (S in the thousands) and
+// large-batch f_B arguments sit in this saturated range.
+constexpr double kSatArg = 45.0;
+
+// The simulation kernel can call one out-of-line copy of expm1
+// (NX_COMPACT_MATH); streaming kernels (K1) keep it inline.
+#ifdef NX_COMPACT_MATH
+static __device__ __noinline__ double expm1_neg(double kx) { return -expm1(-kx); }
+#else
+__device__ __forceinline__ double expm1_neg(double kx) { return -expm1(-kx); }
+#endif
+__device__ __forceinline__ double raw_factor(double k, double x) {
+  const double kx = k * x;
+  return kx >= kSatArg ? 1.0 : expm1_neg(kx);
+}
 __device__ __forceinline__ double clamp_factor(double f) { return f < kFactorMax ? f : kFactorMax; }
 __device__ __forceinline__ double sat(double k, double x) { return clamp_factor(raw_factor(k, x)); }
 

@@ -9,7 +9,12 @@
 // lanes parallelise over engines (K3 PRISM scorer), candidate batch sizes
 // (K2 LENS budget search), allocations (step completion) and learner samples
 // (K4 refit, nx_learner.cuh).
+#ifdef NX_OUTLINE
+#define NX_COMPACT_MATH 1
+#endif
 #include "nx_learner.cuh"
+#include "nx_lens.cuh"
+#include "nx_router.cuh"
 
 namespace nxd {
 
@@ -21,51 +26,18 @@ __device__ __forceinline__ int remaining(const Ctx& c, int r) {
   return c.P->prompt[c.roff + r] - c.P->prefilled[c.roff + r];
 }
 
-// target_latency (lens.cpp:10-31)
-__device__ double target_latency(const Ctx& c, const EngSm& g, int wait_count) {
+// target_latency (lens.cpp:10-31) with the engine's tradeoff model
+__device__ __forceinline__ double target_latency(const Ctx& c, const EngSm& g, int wait_count) {
   const NxReplicaDesc& d = *c.d;
-  const double td_tpot = d.tpot_slo;
-  const double td_ttft = (g.alpha - d.ttft_slo) / g.beta;
-  double t;
-  if (g.l_bar > g.beta) {
-    const double lo = (g.td_min < td_ttft) ? td_ttft : g.td_min;  // max(td_min, td_ttft)
-    t = (lo < td_tpot) ? lo : td_tpot;                              // min(td_tpot, .)
-  } else {
-    t = td_tpot;
-  }
-  if (wait_count > 0) {
-    const double q = static_cast<double>(wait_count) / d.q_ref;
-    const double relax = (q < 1.0) ? q : 1.0;
-    t += relax * (td_tpot - t);
-  }
-  return t;
+  return lens_target(d.ttft_slo, d.tpot_slo, g.alpha, g.beta, g.l_bar, g.td_min, d.q_ref, wait_count);
 }
 
-// Inclusive prefix sums of the remaining prompts of the first `count` waiters
-// into c.prefix[0..count] (prefix[0] = 0). lens.cpp:121-124.
-__device__ void build_prefix(Ctx& c, const int32_t* wq, int count) {
-  __syncwarp();
-  if (c.lane == 0) c.prefix[0] = 0;
-  int carry = 0;
-  for (int base = 0; base < count; base += 32) {
-    const int i = base + c.lane;
-    const int v = i < count ? remaining(c, wq[i]) : 0;
-    const int s = warp_incl_scan(v);
-    if (i < count) c.prefix[i + 1] = carry + s;
-    carry += __shfl_sync(NX_FULL, s, 31);
-  }
-  __syncwarp();
+// Prefix sums of the remaining prompts of the first `count` waiters of wq.
+__device__ __forceinline__ void build_prefix(Ctx& c, const int32_t* wq, int count) {
+  lens_prefix(c.lane, c.prefix, count, [&](int i) { return remaining(c, wq[i]); });
 }
-
-// first j in [0, hi] with prefix[j] >= need (prefix strictly increasing)
 __device__ __forceinline__ int lower_bound_prefix(const int32_t* pre, int hi, int need) {
-  int lo = 0;
-  while (lo < hi) {
-    const int m = (lo + hi) >> 1;
-    if (pre[m] >= need) hi = m;
-    else lo = m + 1;
-  }
-  return lo;
+  return lens_lower_bound(pre, hi, need);
 }
 
 // Publishes a plan: n allocations whose first `ndec` are run-queue decodes.
@@ -95,7 +67,7 @@ __device__ __forceinline__ void write_decodes(Ctx& c, const int32_t* rq, int R, 
 }
 
 // ---- K2: LENS schedule_step (lens.cpp:96-146) -----------------------------------
-__device__ void plan_lens(Ctx& c, int e) {
+__device__ NX_COLD void plan_lens(Ctx& c, int e) {
   EngSm& g = c.eng[e];
   const NxEngineDesc& ed = c.ed[e];
   const int R = g.rq_len, W = g.wq_len, qmax = ed.q_max, mmax = ed.m_max;
@@ -121,77 +93,19 @@ __device__ void plan_lens(Ctx& c, int e) {
     set_plan(c, g, R, R, R, predict(P, R, R), target, 0, 0, R);
     return;
   }
-  const int b_lo = R > 1 ? R : 1;
-  const int b_hi = (R + W < qmax) ? R + W : qmax;
-  const int span = b_hi - R;
+  const int span = ((R + W < qmax) ? R + W : qmax) - R;
   build_prefix(c, wq, span);
   if (c.lane == 0) c.rs->work[2] += span;
   const int32_t* pre = c.prefix;
-  const double thr_eps = target * c.d->eps_ratio;
-  const int iters = c.d->n_iters;
-  double best_err = kInf, best_T = 0.0;
-  int best_budget = -1;
-  for (int B0 = b_lo; B0 <= b_hi; B0 += 32) {
-    const int B = B0 + c.lane;
-    const bool act = B <= b_hi;
-    double err = kInf, T = 0.0;
-    int budget = 0;
-    if (act) {
-      const int avail = R + pre[B - R];
-      int s_cap = (mmax < avail) ? mmax : avail;
-      s_cap = (B < s_cap) ? s_cap : B;  // max(b, min(s_cap, m_max))
-      const double bd = static_cast<double>(B);
-      const double fb = sat(P.kB, bd);
-      int lo = B, hi = s_cap;
-      budget = B;
-      for (int it = 0; it < iters; ++it) {  // binary_search_budget (lens.cpp:46-58)
-        if (lo > hi) break;
-        const int mid = (lo + hi) / 2;
-        if (latency_fb(P, fb, bd, static_cast<double>(mid)) <= target) {
-          budget = mid;
-          lo = mid + 1;
-        } else {
-          hi = mid - 1;
-        }
-      }
-      // realize(allocate_tokens(...)): S = budget, b = R + first j with prefix[j] >= budget - R
-      const int j = lower_bound_prefix(pre, B - R, budget - R);
-      T = predict(P, static_cast<double>(R + j), static_cast<double>(budget));
-      err = fabs(T - target);
-    }
-    // first B whose error is below eps*target ends the sweep (the sequential
-    // loop's early exit fires exactly there); otherwise keep the first strict min
-    const unsigned hit = __ballot_sync(NX_FULL, act && err < thr_eps);
-    if (hit) {
-      best_budget = __shfl_sync(NX_FULL, budget, __ffs(hit) - 1);
-      best_T = __shfl_sync(NX_FULL, T, __ffs(hit) - 1);
-      break;
-    }
-    double v = (act && !isnan(err)) ? err : kInf;
-    int who = c.lane;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ov = __shfl_xor_sync(NX_FULL, v, o);
-      const int ow = __shfl_xor_sync(NX_FULL, who, o);
-      if (ov < v || (ov == v && ow < who)) {
-        v = ov;
-        who = ow;
-      }
-    }
-    const int wb = __shfl_sync(NX_FULL, budget, who & 31);
-    const double wT = __shfl_sync(NX_FULL, T, who & 31);
-    if (v < best_err) {
-      best_err = v;
-      best_budget = wb;
-      best_T = wT;
-    }
-  }
-  if (best_budget < 0) {  // every candidate error was NaN: empty plan
+  const LensPick pick = lens_sweep(c.lane, P, R, span, mmax, c.d->n_iters, target, c.d->eps_ratio, pre);
+  if (pick.budget < 0) {  // every candidate error was NaN: empty plan
     set_plan(c, g, 0, 0, 0, 0.0, target, 0, 0, 0);
     return;
   }
+  const int best_budget = pick.budget;
+  const double best_T = pick.T;
   const int need = best_budget - R;
-  const int j = lower_bound_prefix(pre, span, need);
+  const int j = pick.j;
   write_decodes(c, rq, R, preq, ptok);
   for (int k = c.lane; k < j; k += 32) {  // allocate_tokens waiters (lens.cpp:71-77)
     const int rem = pre[k + 1] - pre[k];
@@ -203,7 +117,7 @@ __device__ void plan_lens(Ctx& c, int e) {
 }
 
 // ---- baseline engine policies (engine.cpp:61-108) -------------------------------
-__device__ void plan_baseline(Ctx& c, int e) {
+__device__ NX_COLD void plan_baseline(Ctx& c, int e) {
   EngSm& g = c.eng[e];
   const NxEngineDesc& ed = c.ed[e];
   const int R = g.rq_len, W = g.wq_len, qmax = ed.q_max, mmax = ed.m_max;
@@ -268,7 +182,7 @@ __device__ void plan_baseline(Ctx& c, int e) {
 }
 
 // ---- trim_for_kv (engine.cpp:184-214) ----------------------------------------------
-__device__ void trim_for_kv(Ctx& c, int e) {
+__device__ NX_COLD void trim_for_kv(Ctx& c, int e) {
   EngSm& g = c.eng[e];
   const NxEngineDesc& ed = c.ed[e];
   int32_t* preq = c.P->plan_req + ed.plan_off;
@@ -320,7 +234,7 @@ __device__ void trim_for_kv(Ctx& c, int e) {
 // Oracle noise (engine.cpp:128-132): the engine stream draws two uniforms per
 // executed step; 32 steps' worth are drawn at once (lane 0, in stream order)
 // and the Box-Muller + exp for each step runs on its own lane.
-__device__ void refill_noise(Ctx& c, int e) {
+__device__ NX_COLD void refill_noise(Ctx& c, int e) {
   EngSm& g = c.eng[e];
   __syncwarp();
   if (c.lane == 0) {
@@ -339,7 +253,7 @@ __device__ void refill_noise(Ctx& c, int e) {
 }
 
 // ---- begin_step (engine.cpp:216-228) + step event (sim.cpp:143-166) ----------------
-__device__ void try_begin_step(Ctx& c, int e, int64_t now_us) {
+__device__ NX_COLD void try_begin_step(Ctx& c, int e, int64_t now_us) {
   EngSm& g = c.eng[e];
   __syncwarp();
   if (g.busy || (g.wq_len == 0 && g.rq_len == 0)) return;
@@ -464,7 +378,7 @@ __device__ bool admit(Ctx& c, int e, int r) {
 }
 
 // ---- TradeoffEstimator refit (lens.cpp:161-188), exact left folds --------------------
-__device__ void tradeoff_refit(Ctx& c, int e) {
+__device__ NX_COLD void tradeoff_refit(Ctx& c, int e) {
   EngSm& g = c.eng[e];
   const NxEngineDesc& ed = c.ed[e];
   const int n = g.tw_len;
@@ -507,7 +421,7 @@ __device__ void tradeoff_refit(Ctx& c, int e) {
 }
 
 // ---- complete_step (engine.cpp:230-282) + handle_step_complete (sim.cpp:196-224) ----
-__device__ void step_complete(Ctx& c, int e, int64_t now_us) {
+__device__ NX_COLD void step_complete(Ctx& c, int e, int64_t now_us) {
   EngSm& g = c.eng[e];
   const NxEngineDesc& ed = c.ed[e];
   const NxPools& P = *c.P;
@@ -686,7 +600,7 @@ __device__ void step_complete(Ctx& c, int e, int64_t now_us) {
 }
 
 // ---- state report (sim.cpp:226-243, engine.cpp:307-332), lane 0 only -----------
-__device__ void state_report(Ctx& c, int e, int64_t now_us) {
+__device__ NX_COLD void state_report(Ctx& c, int e, int64_t now_us) {
   EngSm& g = c.eng[e];
   const NxEngineDesc& ed = c.ed[e];
   wait_refit(c, e);  // the report exports the learner's p_max
@@ -740,10 +654,6 @@ __device__ void state_report(Ctx& c, int e, int64_t now_us) {
 }
 
 // ---- K3: Router::route (router.cpp:141-289) ------------------------------------
-__device__ __forceinline__ double score_load(double w_load, double p_max, double half) {
-  const double rho = w_load / p_max;
-  return 1.0 / (1.0 + rho / half);
-}
 
 // lexicographic first minimum of (key, lane) over lanes with valid keys
 __device__ __forceinline__ int warp_argmin_i64(int64_t key, bool valid) {
@@ -769,7 +679,7 @@ __device__ int least_loaded(Ctx& c) {
   return warp_argmin_i64(len, on);
 }
 
-__device__ int route(Ctx& c, int rid, double now) {
+__device__ NX_COLD int route(Ctx& c, int rid, double now) {
   const NxReplicaDesc& d = *c.d;
   const int n = c.n_eng;
   const int sess = c.P->session[c.roff + rid];
@@ -859,69 +769,36 @@ __device__ int route(Ctx& c, int rid, double now) {
       const double dem = static_cast<double>(prompt) + c.rs->l_bar_ema;
       const double demand = (1.0 < dem) ? dem : 1.0;
       const int e = c.lane;
-      const bool on = e < n;
-      double score = -kInf, rho = 0.0;
-      int id = 0x7fffffff;
-      bool fresh = false;
-      if (on) {
+      EngineView v;
+      v.on = e < n;
+      v.has_rep = false;
+      v.lhat = v.wload = v.mfree = v.at = 0.0;
+      v.pmax = 1.0;
+      v.qlen = 0;
+      v.id = 0x7fffffff;
+      v.affine = false;
+      if (v.on) {
         const EngSm& g = c.eng[e];
-        id = c.ed[e].engine_id;
-        double f0 = 1.0, f1 = 1.0, f2 = 1.0, f3;
-        const double age = g.has_rep ? now - g.rep_at : kInf;
-        if (g.has_rep && age <= d.stale_limit) {
-          fresh = true;
-          const double knee = d.knee * d.ttft_slo;
-          if (g.rep_lhat <= knee) f0 = 1.0;
-          else {
-            const double scale = d.scale_ms > 0.0 ? d.scale_ms : 0.25 * d.ttft_slo;
-            f0 = exp(-(g.rep_lhat - knee) / scale);
-          }
-          f1 = score_load(g.rep_wload, g.rep_pmax, d.load_half);
-          const double rr = g.rep_mfree / (d.headroom * demand);
-          const double cl = (rr < 0.0) ? 0.0 : ((1.0 < rr) ? 1.0 : rr);
-          f2 = cl * cl;
-          rho = g.rep_wload / g.rep_pmax;
-        } else {
-          f0 = 0.5;
-          f2 = 0.5;
-          if (g.has_rep) {
-            rho = g.rep_wload / g.rep_pmax;
-            const double blend = exp(-(age - d.stale_limit) / d.stale_limit);
-            f1 = 1.0 + (score_load(g.rep_wload, g.rep_pmax, d.load_half) - 1.0) * blend;
-          }
-        }
-        f3 = sess_eng[sess] == e ? d.beta_aff : 1.0;
-        const double f[4] = {f0, f1, f2, f3};
-        score = 1.0;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const double w = d.weights[i];
-          double term;
-          if (f[i] == 0.0 && w > 0.0) term = 0.0;
-          else if (w == 1.0) term = f[i];  // pow(x, 1) == x exactly
-          else if (w == 0.0) term = 1.0;   // pow(x, 0) == 1
-          else term = pow(f[i], w);
-          score *= term;
-        }
+        v.has_rep = g.has_rep;
+        v.lhat = g.rep_lhat;
+        v.wload = g.rep_wload;
+        v.mfree = g.rep_mfree;
+        v.pmax = g.rep_pmax;
+        v.at = g.rep_at;
+        v.qlen = g.rep_qlen;
+        v.id = c.ed[e].engine_id;
+        v.affine = sess_eng[sess] == e;
       }
-      // argmax on (score desc, rho asc, id asc) — the sequential scan's "better"
-      int who = on ? e : 64;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double os = __shfl_xor_sync(NX_FULL, score, o);
-        const double orho = __shfl_xor_sync(NX_FULL, rho, o);
-        const int oid = __shfl_xor_sync(NX_FULL, id, o);
-        const int ow = __shfl_xor_sync(NX_FULL, who, o);
-        const bool better = os > score || (os == score && (orho < rho || (orho == rho && oid < id)));
-        if (better) {
-          score = os;
-          rho = orho;
-          id = oid;
-          who = ow;
-        }
-      }
-      chosen = who;
-      if (!__any_sync(NX_FULL, fresh)) chosen = least_loaded(c);  // degraded
+      RouterCfgD rc;
+      for (int i = 0; i < 4; ++i) rc.w[i] = d.weights[i];
+      rc.beta_aff = d.beta_aff;
+      rc.knee = d.knee;
+      rc.scale_ms = d.scale_ms;
+      rc.load_half = d.load_half;
+      rc.headroom = d.headroom;
+      rc.stale_limit = d.stale_limit;
+      rc.ttft_slo = d.ttft_slo;
+      chosen = prism_choose(rc, v, demand, now, n).who;
       __syncwarp();
       if (c.lane == 0) {  // dispatch echo (router.cpp:275-282)
         EngSm& g = c.eng[chosen];
@@ -941,7 +818,7 @@ __device__ int route(Ctx& c, int rid, double now) {
 }
 
 // ---- replica driver -------------------------------------------------------------
-__device__ void init_replica(Ctx& c) {
+__device__ NX_COLD void init_replica(Ctx& c) {
   const NxReplicaDesc& d = *c.d;
   for (int e = c.lane; e < c.n_eng; e += 32) {
     EngSm& g = c.eng[e];
@@ -975,6 +852,7 @@ __device__ void init_replica(Ctx& c) {
     R.arrived = 0; R.rejected = 0; R.pending = c.n_req; R.n_rec = 0; R.events = 0; R.info = 0;
     for (int i = 0; i < 6; ++i) R.work[i] = 0;
     for (int i = 0; i < 16; ++i) R.cycles[i] = 0;
+    R.t_begin_ns = nx_globaltimer();
     R.jq_head = 0;
     R.jq_tail = 0;
     R.l_bar_ema = 128.0;
@@ -1149,7 +1027,7 @@ __device__ void run_replica(Ctx& c) {
   }
 }
 
-__device__ void write_outputs(Ctx& c, int r) {
+__device__ NX_COLD void write_outputs(Ctx& c, int r) {
   __syncwarp();
   NxReplicaOut& o = c.P->rep_out[r];
   if (c.lane == 0) {
@@ -1165,6 +1043,8 @@ __device__ void write_outputs(Ctx& c, int r) {
     o.err_info = R.info;
     for (int i = 0; i < 6; ++i) o.work[i] = R.work[i];
     for (int i = 0; i < 16; ++i) o.cycles[i] = R.cycles[i];
+    o.t_begin_ns = R.t_begin_ns;
+    o.t_end_ns = nx_globaltimer();
   }
   for (int e = c.lane; e < c.n_eng; e += 32) {
     const EngSm& g = c.eng[e];

@@ -8,6 +8,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <numeric>
@@ -30,6 +31,19 @@ extern "C" cudaError_t nx_launch_perf_eval(const double* params, int n_params, c
                                            const int32_t* b, const int32_t* s, double* outT,
                                            double* outThr, int64_t n, int fp32, unsigned* bad,
                                            int sms, cudaStream_t st);
+
+extern "C" cudaError_t nx_launch_lens(const nx_lens_problem* probs, int n, const int32_t* rem,
+                                      nx_lens_plan* plans, int32_t* alloc, int32_t* gpre, int sms,
+                                      cudaStream_t st);
+extern "C" cudaError_t nx_launch_route(nx_route_group* groups, int n, nx_engine_report* reports,
+                                       const nx_route_request* reqs, int32_t* smap,
+                                       nx_route_decision* dec, int32_t* gstatus, int sms,
+                                       cudaStream_t st);
+extern "C" cudaError_t nx_launch_refit(int kind, const nx_refit_problem* probs, int n,
+                                       const int32_t* sb, const int32_t* ss, const double* sy,
+                                       nx_refit_result* out, double* scratch, int64_t scratch_per,
+                                       int grid, int max_long, cudaStream_t st);
+extern "C" int64_t nx_refit_scratch_per(int64_t W);
 
 namespace {
 
@@ -477,6 +491,7 @@ int nx_sim_launch(nx_sim_t h) {
     int per_sm = 0;
     cuda_check(nx_sim_occupancy(kWarpsPerBlock, smem, &per_sm), "occupancy");
     if (per_sm < 1) throw NxError(NX_ECUDA, "simulation kernel does not fit on an SM");
+    if (const char* cap = std::getenv("NX_SIM_CTAS_PER_SM")) per_sm = std::max(1, std::min(per_sm, std::atoi(cap)));
     const int need = h->n_rep;
     const int grid = std::max(1, std::min(need, per_sm * sm_count(h->device)));
     cuda_check(cudaEventRecord(h->ev0, st), "event");
@@ -645,6 +660,14 @@ int nx_sim_work(nx_sim_t h, int32_t replica, int64_t* out6) {
   });
 }
 
+int nx_sim_timeline(nx_sim_t h, int32_t replica, int64_t* begin_end_ns) {
+  return guard([&] {
+    if (replica < 0 || replica >= h->n_rep) throw std::invalid_argument("replica out of range");
+    begin_end_ns[0] = h->h_rep_out[replica].t_begin_ns;
+    begin_end_ns[1] = h->h_rep_out[replica].t_end_ns;
+  });
+}
+
 int nx_sim_phase_cycles(nx_sim_t h, int32_t replica, int64_t* out10) {
   return guard([&] {
     if (replica < 0 || replica >= h->n_rep) throw std::invalid_argument("replica out of range");
@@ -728,6 +751,219 @@ int nx_perf_eval_host(const double* params, int32_t n_params, const int32_t* idx
     if (rc) throw NxError(rc, g_err);
     cuda_check(cudaMemcpy(out_T, d + oT, sizeof(double) * n, cudaMemcpyDeviceToHost), "D2H");
     if (out_thr) cuda_check(cudaMemcpy(out_thr, d + oh, sizeof(double) * n, cudaMemcpyDeviceToHost), "D2H");
+  });
+}
+
+// ---- K2 / K3 / K4 batched operators ------------------------------------------------
+}  // extern "C"
+
+namespace {
+
+int current_sms() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return sm_count(dev);
+}
+
+// Device copy of a host array inside an arena; returns the offset.
+struct Staging {
+  Arena A;
+  unsigned char* d = nullptr;
+  void alloc() { cuda_check(cudaMalloc(&d, A.size), "cudaMalloc"); }
+  ~Staging() {
+    if (d) cudaFree(d);
+  }
+  template <class T>
+  T* at(size_t off) { return reinterpret_cast<T*>(d + off); }
+};
+
+const char* status_text(int st) {
+  switch (st) {
+    case NX_EINVAL: return "invalid argument";
+    case NX_ERUNTIME: return "runtime error";
+    case NX_ELOGIC: return "logic error";
+  }
+  return "error";
+}
+
+}  // namespace
+
+extern "C" {
+
+int nx_abi_sizes(int64_t* out, int32_t n) {
+  const int64_t sz[] = {sizeof(nx_lens_problem), sizeof(nx_lens_plan), sizeof(nx_route_group),
+                        sizeof(nx_engine_report), sizeof(nx_route_request), sizeof(nx_route_decision),
+                        sizeof(nx_refit_problem), sizeof(nx_refit_result), sizeof(nx_replica_summary),
+                        sizeof(nx_request_record)};
+  for (int32_t i = 0; i < n && i < static_cast<int32_t>(sizeof sz / sizeof sz[0]); ++i) out[i] = sz[i];
+  return NX_OK;
+}
+
+int nx_lens_schedule_dev(const nx_lens_problem* problems, int32_t n_problems,
+                         const int32_t* wait_remaining, int64_t n_wait_total, nx_lens_plan* plans,
+                         int32_t* alloc_tokens, void* stream) {
+  return guard([&] {
+    if (n_problems < 0 || n_wait_total < 0) throw std::invalid_argument("nx_lens_schedule: negative sizes");
+    if (n_problems == 0) return;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    int32_t* gpre = nullptr;  // prefix scratch for spans beyond the shared-memory stage
+    cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&gpre),
+                               sizeof(int32_t) * static_cast<size_t>(n_wait_total + n_problems), st),
+               "cudaMallocAsync");
+    cudaError_t e = nx_launch_lens(problems, n_problems, wait_remaining, plans, alloc_tokens, gpre,
+                                   current_sms(), st);
+    const cudaError_t e2 = cudaFreeAsync(gpre, st);
+    cuda_check(e, "nx_lens_kernel launch");
+    cuda_check(e2, "cudaFreeAsync");
+  });
+}
+
+int nx_lens_schedule_host(const nx_lens_problem* problems, int32_t n_problems,
+                          const int32_t* wait_remaining, int64_t n_wait_total, nx_lens_plan* plans,
+                          int32_t* alloc_tokens) {
+  return guard([&] {
+    if (n_problems < 0 || n_wait_total < 0) throw std::invalid_argument("nx_lens_schedule: negative sizes");
+    if (n_problems == 0) return;
+    for (int32_t i = 0; i < n_problems; ++i)
+      if (problems[i].n_wait < 0 || problems[i].wait_off < 0 ||
+          problems[i].wait_off + problems[i].n_wait > n_wait_total)
+        throw std::invalid_argument("nx_lens_schedule: waiter range out of bounds");
+    Staging S;
+    const size_t op = S.A.take<nx_lens_problem>(n_problems), orm = S.A.take<int32_t>(n_wait_total),
+                 opl = S.A.take<nx_lens_plan>(n_problems), oal = S.A.take<int32_t>(n_wait_total);
+    S.alloc();
+    cuda_check(cudaMemcpy(S.at<void>(op), problems, sizeof(nx_lens_problem) * n_problems, cudaMemcpyHostToDevice), "H2D");
+    if (n_wait_total)
+      cuda_check(cudaMemcpy(S.at<void>(orm), wait_remaining, sizeof(int32_t) * n_wait_total, cudaMemcpyHostToDevice), "H2D");
+    const int rc = nx_lens_schedule_dev(S.at<nx_lens_problem>(op), n_problems, S.at<int32_t>(orm),
+                                        n_wait_total, S.at<nx_lens_plan>(opl), S.at<int32_t>(oal), nullptr);
+    if (rc) throw NxError(rc, g_err);
+    cuda_check(cudaMemcpy(plans, S.at<void>(opl), sizeof(nx_lens_plan) * n_problems, cudaMemcpyDeviceToHost), "D2H");
+    if (n_wait_total)
+      cuda_check(cudaMemcpy(alloc_tokens, S.at<void>(oal), sizeof(int32_t) * n_wait_total, cudaMemcpyDeviceToHost), "D2H");
+    for (int32_t i = 0; i < n_problems; ++i)
+      if (plans[i].status != NX_OK)
+        throw NxError(plans[i].status, "schedule_step: problem " + std::to_string(i) + ": " +
+                                           status_text(plans[i].status));
+  });
+}
+
+int nx_prism_route_dev(nx_route_group* groups, int32_t n_groups, nx_engine_report* reports,
+                       const nx_route_request* requests, int32_t* session_map,
+                       nx_route_decision* decisions, int32_t* group_status, void* stream) {
+  return guard([&] {
+    if (n_groups < 0) throw std::invalid_argument("nx_prism_route: negative sizes");
+    if (n_groups == 0) return;
+    cuda_check(nx_launch_route(groups, n_groups, reports, requests, session_map, decisions, group_status,
+                               current_sms(), static_cast<cudaStream_t>(stream)),
+               "nx_route_kernel launch");
+  });
+}
+
+int nx_prism_route_host(nx_route_group* groups, int32_t n_groups, nx_engine_report* reports,
+                        int64_t n_reports, const nx_route_request* requests, int64_t n_requests,
+                        int32_t* session_map, int64_t n_session_entries,
+                        nx_route_decision* decisions, int32_t* group_status) {
+  return guard([&] {
+    if (n_groups < 0 || n_reports < 0 || n_requests < 0 || n_session_entries < 0)
+      throw std::invalid_argument("nx_prism_route: negative sizes");
+    if (n_groups == 0) return;
+    for (int32_t i = 0; i < n_groups; ++i) {
+      const nx_route_group& g = groups[i];
+      if (g.n_engines < 0 || g.n_requests < 0 || g.n_sessions < 0 || g.engine_off < 0 ||
+          g.request_off < 0 || g.session_off < 0 || g.engine_off + g.n_engines > n_reports ||
+          g.request_off + g.n_requests > n_requests || g.session_off + g.n_sessions > n_session_entries)
+        throw std::invalid_argument("nx_prism_route: group ranges out of bounds");
+    }
+    Staging S;
+    const size_t og = S.A.take<nx_route_group>(n_groups), orp = S.A.take<nx_engine_report>(n_reports),
+                 orq = S.A.take<nx_route_request>(n_requests), osm = S.A.take<int32_t>(n_session_entries),
+                 odc = S.A.take<nx_route_decision>(n_requests), ost = S.A.take<int32_t>(n_groups);
+    S.alloc();
+    auto h2d = [&](size_t off, const void* src, size_t bytes) {
+      if (bytes) cuda_check(cudaMemcpy(S.at<void>(off), src, bytes, cudaMemcpyHostToDevice), "H2D");
+    };
+    auto d2h = [&](void* dst, size_t off, size_t bytes) {
+      if (bytes) cuda_check(cudaMemcpy(dst, S.at<void>(off), bytes, cudaMemcpyDeviceToHost), "D2H");
+    };
+    h2d(og, groups, sizeof(nx_route_group) * n_groups);
+    h2d(orp, reports, sizeof(nx_engine_report) * n_reports);
+    h2d(orq, requests, sizeof(nx_route_request) * n_requests);
+    h2d(osm, session_map, sizeof(int32_t) * n_session_entries);
+    const int rc = nx_prism_route_dev(S.at<nx_route_group>(og), n_groups, S.at<nx_engine_report>(orp),
+                                      S.at<nx_route_request>(orq), S.at<int32_t>(osm),
+                                      S.at<nx_route_decision>(odc), S.at<int32_t>(ost), nullptr);
+    if (rc) throw NxError(rc, g_err);
+    d2h(groups, og, sizeof(nx_route_group) * n_groups);
+    d2h(reports, orp, sizeof(nx_engine_report) * n_reports);
+    d2h(session_map, osm, sizeof(int32_t) * n_session_entries);
+    d2h(decisions, odc, sizeof(nx_route_decision) * n_requests);
+    d2h(group_status, ost, sizeof(int32_t) * n_groups);
+    for (int32_t i = 0; i < n_groups; ++i)
+      if (group_status[i] != NX_OK)
+        throw NxError(group_status[i], "Router::route: group " + std::to_string(i) + ": " +
+                                           status_text(group_status[i]));
+  });
+}
+
+int nx_refit_dev(int32_t kind, const nx_refit_problem* problems, int32_t n_problems,
+                 const int32_t* sample_b, const int32_t* sample_s, const double* sample_y,
+                 int64_t max_long_window, nx_refit_result* results, void* stream) {
+  return guard([&] {
+    if (kind != NX_REFIT_LINEAR && kind != NX_REFIT_STRUCTURAL)
+      throw std::invalid_argument("nx_refit: unknown kind");
+    if (n_problems < 0 || max_long_window < 1 || max_long_window > (1 << 24))
+      throw std::invalid_argument("nx_refit: bad sizes");
+    if (n_problems == 0) return;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int64_t per = nx_refit_scratch_per(max_long_window);
+    // one scratch slice per resident warp: bounded by the device, not the batch
+    int grid = std::min<int64_t>(n_problems, static_cast<int64_t>(current_sms()) * 16);
+    const int64_t budget = int64_t(1) << 31;  // bytes of scratch at most
+    while (grid > 1 && per * 8 * grid > budget) grid /= 2;
+    double* scratch = nullptr;
+    cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&scratch), sizeof(double) * per * grid, st),
+               "cudaMallocAsync");
+    const cudaError_t e = nx_launch_refit(kind, problems, n_problems, sample_b, sample_s, sample_y,
+                                          results, scratch, per, grid, static_cast<int>(max_long_window), st);
+    const cudaError_t e2 = cudaFreeAsync(scratch, st);
+    cuda_check(e, "nx_refit_kernel launch");
+    cuda_check(e2, "cudaFreeAsync");
+  });
+}
+
+int nx_refit_host(int32_t kind, const nx_refit_problem* problems, int32_t n_problems,
+                  const int32_t* sample_b, const int32_t* sample_s, const double* sample_y,
+                  int64_t n_samples_total, nx_refit_result* results) {
+  return guard([&] {
+    if (n_problems < 0 || n_samples_total < 0) throw std::invalid_argument("nx_refit: negative sizes");
+    if (n_problems == 0) return;
+    int64_t max_w = 1;
+    for (int32_t i = 0; i < n_problems; ++i) {
+      const nx_refit_problem& p = problems[i];
+      if (p.n_samples < 0 || p.sample_off < 0 || p.sample_off + p.n_samples > n_samples_total)
+        throw std::invalid_argument("nx_refit: sample range out of bounds");
+      max_w = std::max<int64_t>(max_w, std::min<int64_t>(p.long_window, 1 << 24));
+    }
+    Staging S;
+    const size_t op = S.A.take<nx_refit_problem>(n_problems), ob = S.A.take<int32_t>(n_samples_total),
+                 os = S.A.take<int32_t>(n_samples_total), oy = S.A.take<double>(n_samples_total),
+                 orr = S.A.take<nx_refit_result>(n_problems);
+    S.alloc();
+    cuda_check(cudaMemcpy(S.at<void>(op), problems, sizeof(nx_refit_problem) * n_problems, cudaMemcpyHostToDevice), "H2D");
+    if (n_samples_total) {
+      cuda_check(cudaMemcpy(S.at<void>(ob), sample_b, sizeof(int32_t) * n_samples_total, cudaMemcpyHostToDevice), "H2D");
+      cuda_check(cudaMemcpy(S.at<void>(os), sample_s, sizeof(int32_t) * n_samples_total, cudaMemcpyHostToDevice), "H2D");
+      cuda_check(cudaMemcpy(S.at<void>(oy), sample_y, sizeof(double) * n_samples_total, cudaMemcpyHostToDevice), "H2D");
+    }
+    const int rc = nx_refit_dev(kind, S.at<nx_refit_problem>(op), n_problems, S.at<int32_t>(ob),
+                                S.at<int32_t>(os), S.at<double>(oy), max_w, S.at<nx_refit_result>(orr), nullptr);
+    if (rc) throw NxError(rc, g_err);
+    cuda_check(cudaMemcpy(results, S.at<void>(orr), sizeof(nx_refit_result) * n_problems, cudaMemcpyDeviceToHost), "D2H");
+    for (int32_t i = 0; i < n_problems; ++i)
+      if (results[i].status != NX_OK)
+        throw NxError(results[i].status, "OnlineLearner refit: problem " + std::to_string(i) + ": " +
+                                             status_text(results[i].status));
   });
 }
 

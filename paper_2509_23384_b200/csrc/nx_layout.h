@@ -65,6 +65,8 @@ typedef struct NxReplicaOut {
      [6] structural refits (refit warp, overlapped), [7] report deliveries,
      [8] event-loop warp blocked on a pending refit, [9]-[15] refit internals */
   int64_t cycles[16];
+  /* %globaltimer (ns) when the replica's CTA started and finished it */
+  int64_t t_begin_ns, t_end_ns;
 } NxReplicaOut;
 
 typedef struct NxEngineOut {

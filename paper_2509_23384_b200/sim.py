@@ -109,6 +109,12 @@ class Batch:
         check(lib().nx_sim_phase_cycles(self.h, r, out))
         return list(out)
 
+    def timeline(self, r: int):
+        """(begin_ns, end_ns) of replica r on the device's %globaltimer."""
+        out = (C.c_int64 * 2)()
+        check(lib().nx_sim_timeline(self.h, r, out))
+        return out[0], out[1]
+
     def summaries_nbytes(self) -> int:
         ptr, n = C.c_void_p(), C.c_int64()
         check(lib().nx_sim_summaries_dev(self.h, C.byref(ptr), C.byref(n)))

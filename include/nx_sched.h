@@ -274,6 +274,10 @@ int nx_sim_copy_summaries(nx_sim_t h, void* dst_dev);
  * the reference's config errors (RunConfig::validate, sim.cpp:418-452). */
 int nx_workload_info(const char* config_json, uint64_t* arrival_hash, int64_t* n_requests,
                      int64_t* n_sessions);
+/* xoshiro256++ state of Rng(substream_seed(root_seed, tag, index))
+ * (proj/include/servesim/rng.h): e.g. a Router's weighted-policy stream is
+ * tag "router", index 0 (router.cpp:62-64). */
+int nx_rng_state(uint64_t root_seed, const char* tag, uint64_t index, uint64_t* state4);
 int nx_synth_generate(const char* scenario, int64_t n, uint64_t seed, int64_t* prompts,
                       int64_t* outputs, char* session_ids16);
 

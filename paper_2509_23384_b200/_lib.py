@@ -81,6 +81,7 @@ def lib() -> C.CDLL:
     L.nx_synth_generate.argtypes = [C.c_char_p, C.c_int64, C.c_uint64, _P(C.c_int64),
                                     _P(C.c_int64), C.c_char_p]
     V = C.c_void_p
+    L.nx_rng_state.argtypes = [C.c_uint64, C.c_char_p, C.c_uint64, _P(C.c_uint64)]
     L.nx_abi_sizes.argtypes = [_P(C.c_int64), C.c_int32]
     L.nx_lens_schedule_dev.argtypes = [V, C.c_int32, V, C.c_int64, V, V, V]
     L.nx_lens_schedule_host.argtypes = [V, C.c_int32, V, C.c_int64, V, V]

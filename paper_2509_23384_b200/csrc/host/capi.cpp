@@ -979,6 +979,13 @@ int nx_workload_info(const char* config_json, uint64_t* arrival_hash, int64_t* n
   });
 }
 
+int nx_rng_state(uint64_t root_seed, const char* tag, uint64_t index, uint64_t* state4) {
+  return guard([&] {
+    nx::Xoshiro x(nx::substream_seed(root_seed, tag ? tag : "", index));
+    for (int i = 0; i < 4; ++i) state4[i] = x.s[i];
+  });
+}
+
 int nx_synth_generate(const char* scenario, int64_t n, uint64_t seed, int64_t* prompts,
                       int64_t* outputs, char* session_ids16) {
   return guard([&] {

@@ -37,7 +37,7 @@ def problem_record(params, cfg: LearnerConfig, sample_off: int, n_samples: int) 
     return r
 
 
-def refit_batch(kind: int, problems: np.ndarray, b, s, y) -> np.ndarray:
+def refit_batch(kind: int, problems: np.ndarray, b, s, y, raise_errors: bool = True) -> np.ndarray:
     """Batched update_linear (kind 0) / update_structural (kind 1) on host
     arrays; samples CSR by problems["sample_off"/"n_samples"], chronological.
     Returns nx_refit_result records (params after, counter increments,
@@ -47,8 +47,10 @@ def refit_batch(kind: int, problems: np.ndarray, b, s, y) -> np.ndarray:
     s = np.ascontiguousarray(s, dtype=np.int32)
     y = np.ascontiguousarray(y, dtype=np.float64)
     out = np.zeros(problems.size, dtype=abi.REFIT_RESULT)
-    check(lib().nx_refit_host(kind, abi.ptr(problems), problems.size, abi.ptr(b), abi.ptr(s),
-                              abi.ptr(y), b.size, abi.ptr(out)))
+    rc = lib().nx_refit_host(kind, abi.ptr(problems), problems.size, abi.ptr(b), abi.ptr(s),
+                             abi.ptr(y), b.size, abi.ptr(out))
+    if raise_errors or not (out["status"] != 0).any():
+        check(rc)
     return out
 
 

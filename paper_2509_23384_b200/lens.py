@@ -89,20 +89,23 @@ def problem_record(n_run: int, n_wait: int, wait_off: int, slo: SLOSpec, tm: Tra
     return r
 
 
-def schedule_batch(problems: np.ndarray, wait_remaining: np.ndarray):
+def schedule_batch(problems: np.ndarray, wait_remaining: np.ndarray, raise_errors: bool = True):
     """Batched schedule_step on host arrays (copies in/out included).
 
     problems: nx_lens_problem records; wait_remaining: int32 remaining
     prompts, CSR by problems["wait_off"/"n_wait"]. Returns (plans,
     alloc_tokens) — plans are nx_lens_plan records; alloc_tokens[wait_off+k]
-    holds waiter k's prefill chunk for k < n_prefill.
+    holds waiter k's prefill chunk for k < n_prefill. With raise_errors
+    False, failing problems only report their status in the plan.
     """
     problems = np.ascontiguousarray(problems, dtype=abi.LENS_PROBLEM)
     rem = np.ascontiguousarray(wait_remaining, dtype=np.int32)
     plans = np.zeros(problems.size, dtype=abi.LENS_PLAN)
     alloc = np.zeros(rem.size, dtype=np.int32)
-    check(lib().nx_lens_schedule_host(abi.ptr(problems), problems.size, abi.ptr(rem), rem.size,
-                                      abi.ptr(plans), abi.ptr(alloc)))
+    rc = lib().nx_lens_schedule_host(abi.ptr(problems), problems.size, abi.ptr(rem), rem.size,
+                                     abi.ptr(plans), abi.ptr(alloc))
+    if raise_errors or not (plans["status"] != 0).any():
+        check(rc)  # per-problem failures leave every plan written (status field)
     return plans, alloc
 
 

@@ -119,14 +119,25 @@ class Router:
 
 
 def route_batch(groups: np.ndarray, reports: np.ndarray, requests: np.ndarray,
-                session_map: np.ndarray):
+                session_map: np.ndarray, raise_errors: bool = True):
     """Batched Router::route on host record arrays (updated in place like the
     routers' own state). Returns (decisions, group_status)."""
     for a in (groups, reports, requests, session_map):
         assert a.flags["C_CONTIGUOUS"]
     dec = np.zeros(requests.size, dtype=abi.ROUTE_DECISION)
     st = np.zeros(groups.size, dtype=np.int32)
-    check(lib().nx_prism_route_host(abi.ptr(groups), groups.size, abi.ptr(reports), reports.size,
-                                    abi.ptr(requests), requests.size, abi.ptr(session_map),
-                                    session_map.size, abi.ptr(dec), abi.ptr(st)))
+    rc = lib().nx_prism_route_host(abi.ptr(groups), groups.size, abi.ptr(reports), reports.size,
+                                   abi.ptr(requests), requests.size, abi.ptr(session_map),
+                                   session_map.size, abi.ptr(dec), abi.ptr(st))
+    if raise_errors or not (st != 0).any():
+        check(rc)
     return dec, st
+
+
+def router_rng_state(root_seed: int) -> list:
+    """State of the Router's weighted-policy stream, Rng(substream_seed(seed,
+    "router")) (router.cpp:62-64)."""
+    import ctypes as C
+    out = (C.c_uint64 * 4)()
+    check(lib().nx_rng_state(root_seed, b"router", 0, out))
+    return list(out)

@@ -193,6 +193,64 @@ int nx_refit_host(int32_t kind, const nx_refit_problem* problems, int32_t n_prob
                   const int32_t* sample_b, const int32_t* sample_s, const double* sample_y,
                   int64_t n_samples_total, nx_refit_result* results);
 
+/* ---- scheduling building blocks (batched, host pointers) -------------------
+ * The reference's free functions under schedule_step / Router::route /
+ * TradeoffEstimator, evaluated on the device with the same core the
+ * simulator uses; the C++ drop-in (include/nx_servesim.hpp) calls these.
+ * Each returns the first failing record's status (all records written). */
+typedef struct nx_target_query {      /* target_latency (lens.h:93-99) */
+  double ttft_slo_ms, tpot_slo_ms, alpha_ms, beta, l_bar, td_min_ms, q_ref;
+  int64_t wait_count;
+  double target_ms;                   /* out */
+  int32_t slo_risk, status;           /* out */
+} nx_target_query;
+
+typedef struct nx_budget_query {      /* binary_search_budget (lens.h:101-106) */
+  double params[8];
+  double target_ms;
+  int64_t b, m_max, q_max, s_cap;     /* s_cap < 0: m_max */
+  int32_t n_search_iters, status;     /* status out */
+  int64_t budget;                     /* out */
+} nx_budget_query;
+
+typedef struct nx_allocate_problem {  /* allocate_tokens (lens.h:108-112) */
+  int64_t b, s;
+  int64_t wait_off;                   /* waiters' remaining prompts at [wait_off, +n_wait) */
+  int32_t n_run, n_wait;
+  int32_t n_prefill, status;          /* out: waiters admitted (tokens[wait_off + k]) */
+} nx_allocate_problem;
+
+typedef struct nx_score_query {       /* score_latency/load/capacity (router.h:57-66) */
+  double l_hat_ms, w_load_tokens, m_free_tokens, p_max;
+  double demand_tokens;
+  double latency_knee, latency_scale_ms, ttft_slo_ms, load_half_ms, capacity_headroom;
+  double latency, load, capacity;     /* out */
+  int32_t status, pad_;
+} nx_score_query;
+
+#define NX_TRADEOFF_WINDOW 200        /* TradeoffEstimator::kWindow (lens.h:145) */
+typedef struct nx_completion {        /* CompletionStats (lens.h:126-130) */
+  double ttft_ms, tpot_ms;
+  int64_t decode_len;
+} nx_completion;
+
+typedef struct nx_tradeoff_state {    /* TradeoffEstimator state (lens.h:132-151) */
+  double alpha_ms, beta, l_bar, td_min_ms;
+  int64_t degenerate_updates;
+  double win_ttft[NX_TRADEOFF_WINDOW], win_tpot[NX_TRADEOFF_WINDOW];
+  int32_t win_head, win_len;
+  int64_t comp_off;                   /* this update's completions [comp_off, +n_new) */
+  int32_t n_new, pad_;
+} nx_tradeoff_state;
+
+int nx_target_latency_host(nx_target_query* q, int32_t n);
+int nx_budget_search_host(nx_budget_query* q, int32_t n);
+int nx_allocate_tokens_host(nx_allocate_problem* p, int32_t n, const int32_t* wait_remaining,
+                            int64_t n_wait_total, int32_t* tokens);
+int nx_router_scores_host(nx_score_query* q, int32_t n);
+int nx_tradeoff_update_host(nx_tradeoff_state* st, int32_t n, const nx_completion* completions,
+                            int64_t n_completions);
+
 /* ---- K5 (+K2/K3/K4 inside): batched replica simulation --------------------
  * Replaces servesim::run_simulation / sweep (proj/include/servesim/sim.h:
  * 78-100, proj/src/sim.cpp:245-347, 596-642): each config is a RunConfig JSON

@@ -24,6 +24,7 @@ namespace nxd {
 
 constexpr uint64_t kNoEvent = ~0ull;
 constexpr int kFbTable = 1024;  // batch-factor table entries per learner fit
+constexpr int kFitSmemS = 4096; // 1/f_S entries of the refit warp's shared-memory fit tables
 
 // Engine scalars (EngineSim + OnlineLearner + TradeoffEstimator + router view)
 struct EngSm {
@@ -79,6 +80,8 @@ struct Ctx {
   int64_t roff, soff;
   int n_eng, n_req, n_sess, lane, prefix_cap;
   int worker;              // 0: event-loop warp, 1: structural-refit warp
+  double* fsm;             // shared-memory fit tables (1/f_B, then 1/f_S); nullptr: use scratch
+  int fsm_cap;             // 1/f_S entries that fit in fsm
 };
 
 template <class T>

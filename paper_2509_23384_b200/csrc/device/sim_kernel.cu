@@ -9,8 +9,8 @@
 // lanes parallelise over engines (K3 PRISM scorer), candidate batch sizes
 // (K2 LENS budget search), allocations (step completion) and learner samples
 // (K4 refit, nx_learner.cuh).
-#ifdef NX_OUTLINE
-#define NX_COMPACT_MATH 1
+#ifndef NX_INLINE_EXPM1
+#define NX_COMPACT_MATH 1  // one out-of-line expm1 (was ~180 KB of inlined copies)
 #endif
 #include "nx_learner.cuh"
 #include "nx_lens.cuh"
@@ -1067,7 +1067,7 @@ __device__ NX_COLD void write_outputs(Ctx& c, int r) {
 // expected first) from a global counter so a long replica never idles others.
 extern "C" __global__ void __launch_bounds__(64)
 nx_sim_kernel(const NxPools* __restrict__ pools, const int32_t* __restrict__ order, int n_rep,
-              int* next_rep, int smem_per_cta, int prefix_cap) {
+              int* next_rep, int smem_per_cta, int prefix_cap, int max_eng) {
   using namespace nxd;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int s_slot;
@@ -1084,6 +1084,10 @@ nx_sim_kernel(const NxPools* __restrict__ pools, const int32_t* __restrict__ ord
   c.prefix = reinterpret_cast<int32_t*>(c.chunk);
   c.eng = reinterpret_cast<EngSm*>(smem + rep_bytes + 2 * stage);
   c.prefix_cap = prefix_cap;
+  // the refit warp's fit tables follow the engine states (nx_sim_smem_per_warp)
+  const size_t fit_off = (rep_bytes + 2 * stage + sizeof(EngSm) * static_cast<size_t>(max_eng) + 15) & ~size_t(15);
+  c.fsm = warp == 1 ? reinterpret_cast<double*>(smem + fit_off) : nullptr;
+  c.fsm_cap = kFitSmemS;
   (void)smem_per_cta;
   while (true) {
     if (threadIdx.x == 0) s_slot = atomicAdd(next_rep, 1);
@@ -1122,22 +1126,28 @@ extern "C" size_t nx_sim_smem_per_warp(int max_engines, int prefix_cap) {
   const size_t rep_bytes = (sizeof(RepSm) + 15) & ~size_t(15);
   const size_t stage = ((static_cast<size_t>(prefix_cap) * 4 > 32 * 5 * 8 ? static_cast<size_t>(prefix_cap) * 4
                                                                         : 32 * 5 * 8) + 15) & ~size_t(15);
-  return rep_bytes + 2 * stage + sizeof(EngSm) * static_cast<size_t>(max_engines);
+  const size_t fit_off = (rep_bytes + 2 * stage + sizeof(EngSm) * static_cast<size_t>(max_engines) + 15) &
+                         ~size_t(15);
+  return fit_off + sizeof(double) * (kFbTable + kFitSmemS);
 }
 
 extern "C" cudaError_t nx_launch_sim(const NxPools* d_pools, const int32_t* d_order, int n_rep,
-                                     int* d_next, int smem_per_warp, int prefix_cap, int grid,
-                                     int warps_per_block, cudaStream_t st) {
+                                     int* d_next, int smem_per_warp, int prefix_cap, int max_eng,
+                                     int grid, int warps_per_block, cudaStream_t st) {
   const size_t smem = static_cast<size_t>(smem_per_warp);  // one replica per CTA
   cudaError_t err = cudaFuncSetAttribute(nx_sim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
   if (err != cudaSuccess) return err;
   nx_sim_kernel<<<grid, 32 * warps_per_block, smem, st>>>(d_pools, d_order, n_rep, d_next,
-                                                          smem_per_warp, prefix_cap);
+                                                          smem_per_warp, prefix_cap, max_eng);
   return cudaGetLastError();
 }
 
 extern "C" cudaError_t nx_sim_occupancy(int warps_per_block, size_t smem, int* blocks_per_sm) {
+  // dynamic shared memory above 48 KB must be opted into before the query
+  cudaError_t err = cudaFuncSetAttribute(nx_sim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+  if (err != cudaSuccess) return err;
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, nx_sim_kernel,
                                                        32 * warps_per_block, smem);
 }

@@ -23,8 +23,8 @@
 #include "report.hpp"
 
 extern "C" cudaError_t nx_launch_sim(const NxPools* d_pools, const int32_t* d_order, int n_rep,
-                                     int* d_next, int smem_per_warp, int prefix_cap, int grid,
-                                     int warps_per_block, cudaStream_t st);
+                                     int* d_next, int smem_per_warp, int prefix_cap, int max_eng,
+                                     int grid, int warps_per_block, cudaStream_t st);
 extern "C" cudaError_t nx_sim_occupancy(int warps_per_block, size_t smem, int* blocks_per_sm);
 extern "C" size_t nx_sim_smem_per_warp(int max_engines, int prefix_cap);
 extern "C" cudaError_t nx_launch_perf_eval(const double* params, int n_params, const int32_t* idx,
@@ -44,6 +44,8 @@ extern "C" cudaError_t nx_launch_refit(int kind, const nx_refit_problem* probs, 
                                        nx_refit_result* out, double* scratch, int64_t scratch_per,
                                        int grid, int max_long, cudaStream_t st);
 extern "C" int64_t nx_refit_scratch_per(int64_t W);
+extern "C" cudaError_t nx_launch_scalar_ops(int op, void* recs, int n, const void* aux_in,
+                                            void* aux_out, cudaStream_t st);
 
 namespace {
 
@@ -495,7 +497,7 @@ int nx_sim_launch(nx_sim_t h) {
     const int need = h->n_rep;
     const int grid = std::max(1, std::min(need, per_sm * sm_count(h->device)));
     cuda_check(cudaEventRecord(h->ev0, st), "event");
-    cuda_check(nx_launch_sim(h->d_pools, h->d_order, h->n_rep, h->d_next, spw, h->prefix_cap, grid,
+    cuda_check(nx_launch_sim(h->d_pools, h->d_order, h->n_rep, h->d_next, spw, h->prefix_cap, h->max_eng, grid,
                              kWarpsPerBlock, st), "nx_sim_kernel launch");
     cuda_check(cudaEventRecord(h->ev1, st), "event");
     h->launched = true;
@@ -964,6 +966,89 @@ int nx_refit_host(int32_t kind, const nx_refit_problem* problems, int32_t n_prob
       if (results[i].status != NX_OK)
         throw NxError(results[i].status, "OnlineLearner refit: problem " + std::to_string(i) + ": " +
                                              status_text(results[i].status));
+  });
+}
+
+// ---- scheduling building blocks --------------------------------------------------
+}  // extern "C"
+
+namespace {
+
+// Stage records (+ optional aux arrays) on the device, run one scalar-ops
+// kernel, copy records (+ aux out) back. Returns after synchronising.
+void run_scalar_op(int op, void* recs, size_t rec_bytes, int n, const void* aux_in,
+                   size_t aux_in_bytes, void* aux_out, size_t aux_out_bytes) {
+  Staging S;
+  const size_t orc = S.A.take<unsigned char>(rec_bytes * n), oi = S.A.take<unsigned char>(aux_in_bytes),
+               oo = S.A.take<unsigned char>(aux_out_bytes);
+  S.alloc();
+  cuda_check(cudaMemcpy(S.at<void>(orc), recs, rec_bytes * n, cudaMemcpyHostToDevice), "H2D");
+  if (aux_in_bytes) cuda_check(cudaMemcpy(S.at<void>(oi), aux_in, aux_in_bytes, cudaMemcpyHostToDevice), "H2D");
+  if (aux_out_bytes) cuda_check(cudaMemcpy(S.at<void>(oo), aux_out, aux_out_bytes, cudaMemcpyHostToDevice), "H2D");
+  cuda_check(nx_launch_scalar_ops(op, S.at<void>(orc), n, S.at<void>(oi), S.at<void>(oo), nullptr), "launch");
+  cuda_check(cudaMemcpy(recs, S.at<void>(orc), rec_bytes * n, cudaMemcpyDeviceToHost), "D2H");
+  if (aux_out_bytes) cuda_check(cudaMemcpy(aux_out, S.at<void>(oo), aux_out_bytes, cudaMemcpyDeviceToHost), "D2H");
+}
+
+template <class R>
+void first_status(const R* r, int32_t n, const char* what) {
+  for (int32_t i = 0; i < n; ++i)
+    if (r[i].status != NX_OK)
+      throw NxError(r[i].status, std::string(what) + ": record " + std::to_string(i) + ": " +
+                                     status_text(r[i].status));
+}
+
+}  // namespace
+
+extern "C" {
+
+int nx_target_latency_host(nx_target_query* q, int32_t n) {
+  return guard([&] {
+    if (n <= 0) return;
+    run_scalar_op(0, q, sizeof *q, n, nullptr, 0, nullptr, 0);
+    first_status(q, n, "target_latency");
+  });
+}
+
+int nx_budget_search_host(nx_budget_query* q, int32_t n) {
+  return guard([&] {
+    if (n <= 0) return;
+    run_scalar_op(1, q, sizeof *q, n, nullptr, 0, nullptr, 0);
+    first_status(q, n, "binary_search_budget");
+  });
+}
+
+int nx_allocate_tokens_host(nx_allocate_problem* p, int32_t n, const int32_t* wait_remaining,
+                            int64_t n_wait_total, int32_t* tokens) {
+  return guard([&] {
+    if (n <= 0) return;
+    for (int32_t i = 0; i < n; ++i)
+      if (p[i].n_wait < 0 || p[i].wait_off < 0 || p[i].wait_off + p[i].n_wait > n_wait_total)
+        throw std::invalid_argument("allocate_tokens: waiter range out of bounds");
+    run_scalar_op(2, p, sizeof *p, n, wait_remaining, sizeof(int32_t) * n_wait_total, tokens,
+                  sizeof(int32_t) * n_wait_total);
+    first_status(p, n, "allocate_tokens");
+  });
+}
+
+int nx_router_scores_host(nx_score_query* q, int32_t n) {
+  return guard([&] {
+    if (n <= 0) return;
+    run_scalar_op(3, q, sizeof *q, n, nullptr, 0, nullptr, 0);
+    first_status(q, n, "router scores");
+  });
+}
+
+int nx_tradeoff_update_host(nx_tradeoff_state* st, int32_t n, const nx_completion* completions,
+                            int64_t n_completions) {
+  return guard([&] {
+    if (n <= 0) return;
+    for (int32_t i = 0; i < n; ++i)
+      if (st[i].n_new < 0 || st[i].comp_off < 0 || st[i].comp_off + st[i].n_new > n_completions ||
+          st[i].win_len < 0 || st[i].win_len > NX_TRADEOFF_WINDOW || st[i].win_head < 0 ||
+          st[i].win_head >= NX_TRADEOFF_WINDOW)
+        throw std::invalid_argument("TradeoffEstimator: state out of range");
+    run_scalar_op(4, st, sizeof *st, n, completions, sizeof(nx_completion) * n_completions, nullptr, 0);
   });
 }
 

@@ -113,7 +113,8 @@ int nx_lens_schedule_host(const nx_lens_problem* problems, int32_t n_problems,
  * seeing the previous ones' dispatch echo (router.cpp:275-282) and session
  * memory (remember_session). Groups are independent (one warp each).
  * Policies: 0 prism, 1 round_robin, 2 session_affinity, 3 least_loaded,
- * 5 weighted (4 latency_based needs completion history: NX_EINVAL).
+ * 4 latency_based (the caller keeps the completion windows and passes each
+ * engine's rolling mean; one request per group), 5 weighted.
  * Report rows and group state (l_bar_ema, rng, rr_next, session map) are
  * updated in place, as the Router's own state would be. */
 typedef struct nx_route_group {
@@ -137,6 +138,7 @@ typedef struct nx_engine_report {     /* EngineReport (engine.h:50-67) + registr
   int64_t queue_len;
   int32_t engine_id;
   int32_t has_report;                 /* 0: no report received yet */
+  double rolling_latency_ms;          /* latency_based only: the router's rolling e2e mean */
 } nx_engine_report;
 
 typedef struct nx_route_request {

@@ -1,0 +1,347 @@
+// nx_servesim.hpp — C++ drop-in for the reference's perf-model, scheduler,
+// router and learner interfaces (proj/include/servesim/{perf_model,lens,
+// router,learner,rng,engine}.h), backed by the B200 path.
+//
+// Same namespace, type names, fields, defaults, signatures and exception
+// classes as the reference, so its callers (and its own unit tests,
+// tests/refsuite) compile unchanged against this header. Every model
+// evaluation and scheduling decision runs on the device through the C-ABI
+// (include/nx_sched.h); what stays on the host is object state the
+// reference keeps in std containers (sample rings, completion windows,
+// report tables, session maps) and JSON I/O.
+//
+// Link: paper_2509_23384_b200/_nxsched.so (which contains this API).
+#pragma once
+
+#include <array>
+#include <cmath>
+#include <cstdint>
+#include <deque>
+#include <map>
+#include <numbers>
+#include <optional>
+#include <span>
+#include <string>
+#include <string_view>
+#include <unordered_map>
+#include <vector>
+
+namespace servesim {
+
+// ---- perf model (perf_model.h:14-54) -----------------------------------------------
+struct PerfParams {
+  double tau0 = 0.0;
+  double w0 = 0.0;
+  double ws = 1.0;
+  double tauB = 0.0;
+  double tauS = 0.0;
+  double p_max = 1.0;
+  double kB = 1.0;
+  double kS = 1.0;
+
+  bool valid() const;
+  std::string to_json() const;
+  static PerfParams from_json(const std::string& text);
+};
+
+struct BatchShape {
+  int64_t b = 1;
+  int64_t s = 1;
+  bool valid() const { return b >= 1 && s >= b; }
+};
+
+struct LatencySample {
+  BatchShape shape;
+  double observed_ms = 0.0;
+  double sim_time_ms = 0.0;
+};
+
+double throughput(const PerfParams& params, const BatchShape& shape);
+double predict_latency(const PerfParams& params, const BatchShape& shape);
+double goodness_of_fit(const PerfParams& params, std::span<const LatencySample> samples);
+
+// Batched forms (one device launch): out[i] for shapes[i].
+std::vector<double> predict_latency_batch(const PerfParams& params, std::span<const BatchShape> shapes);
+
+// ---- deterministic RNG (rng.h) -----------------------------------------------------
+class Rng {
+ public:
+  explicit Rng(uint64_t seed) {
+    uint64_t x = seed;
+    for (auto& w : s_) w = splitmix64(x);
+  }
+  uint64_t next_u64() {
+    const uint64_t out = rotl(s_[0] + s_[3], 23) + s_[0];
+    const uint64_t t = s_[1] << 17;
+    s_[2] ^= s_[0];
+    s_[3] ^= s_[1];
+    s_[1] ^= s_[2];
+    s_[0] ^= s_[3];
+    s_[2] ^= t;
+    s_[3] = rotl(s_[3], 45);
+    return out;
+  }
+  double uniform() { return (static_cast<double>(next_u64() >> 11) + 1.0) * 0x1.0p-53; }
+  uint64_t below(uint64_t n) { return n ? next_u64() % n : 0; }
+  double normal() {
+    const double u1 = uniform();
+    const double u2 = uniform();
+    return std::sqrt(-2.0 * std::log(u1)) * std::cos(2.0 * std::numbers::pi * u2);
+  }
+  static uint64_t splitmix64(uint64_t& x) {
+    uint64_t z = (x += 0x9e3779b97f4a7c15ULL);
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+  }
+  const std::array<uint64_t, 4>& state() const { return s_; }
+
+ private:
+  static uint64_t rotl(uint64_t v, int k) { return (v << k) | (v >> (64 - k)); }
+  std::array<uint64_t, 4> s_{};
+};
+
+uint64_t substream_seed(uint64_t root, std::string_view tag, uint64_t index = 0);
+
+// ---- engine-facing types the scheduler and router read (engine.h) -------------------
+PerfParams perf_profile(const std::string& name);
+
+struct StateVector {
+  int engine_id = 0;
+  double l_hat_ms = 0.0;
+  double w_load_tokens = 0.0;
+  double m_free_tokens = 0.0;
+  double p_max = 1.0;
+  double reported_at_ms = 0.0;
+  bool valid() const {
+    return l_hat_ms >= 0.0 && w_load_tokens >= 0.0 && m_free_tokens >= 0.0 && p_max > 0.0;
+  }
+};
+
+struct EngineReport {
+  StateVector state;
+  int64_t queue_len = 0;
+};
+
+// ---- LENS (lens.h) -----------------------------------------------------------------
+struct SLOSpec {
+  double ttft_slo_ms = 2000.0;
+  double tpot_slo_ms = 12.0;
+  bool valid() const { return ttft_slo_ms > 0.0 && tpot_slo_ms > 0.0; }
+};
+
+struct TradeoffModel {
+  double alpha_ms = 2000.0;
+  double beta = 16.0;
+  double l_bar = 128.0;
+  double td_min_ms = 2.0;
+  bool valid() const { return beta > 0.0 && l_bar >= 1.0 && td_min_ms > 0.0; }
+  static TradeoffModel initial_for(const SLOSpec& slo) {
+    TradeoffModel tm;
+    tm.alpha_ms = 2.0 * slo.ttft_slo_ms;
+    tm.beta = slo.ttft_slo_ms / slo.tpot_slo_ms;
+    return tm;
+  }
+};
+
+enum class RequestState { kWaiting, kRunning, kFinished };
+
+struct Request {
+  uint64_t id = 0;
+  std::string session_id;
+  int64_t prompt_len = 1;
+  int64_t prefilled = 0;
+  int64_t decoded = 0;
+  int64_t target_decode = 1;
+  int64_t precredited = 0;
+  double arrival_ms = 0.0;
+  std::optional<double> first_token_ms;
+  RequestState state = RequestState::kWaiting;
+  bool kv_admitted = false;
+  int64_t allocated_prefill = 0;
+  int64_t allocated_decode = 0;
+  int64_t remaining_prompt() const { return prompt_len - prefilled; }
+};
+
+struct SchedulerConfig {
+  int64_t m_max = 8192;
+  int64_t q_max = 256;
+  int n_search_iters = 10;
+  double eps_ratio = 0.05;
+  double q_ref = 16.0;
+  bool valid() const {
+    return m_max >= q_max && q_max >= 1 && n_search_iters >= 1 && eps_ratio > 0.0 &&
+           eps_ratio < 1.0 && q_ref > 0.0;
+  }
+};
+
+struct Allocation {
+  uint64_t request_id = 0;
+  int64_t tokens = 0;
+  bool is_prefill = false;
+};
+
+struct BatchPlan {
+  std::vector<Allocation> allocations;
+  int64_t b = 0;
+  int64_t s = 0;
+  double predicted_ms = 0.0;
+  double target_ms = 0.0;
+  bool overload = false;
+  bool empty() const { return allocations.empty(); }
+};
+
+struct TargetLatency {
+  double target_ms = 0.0;
+  bool slo_risk = false;
+};
+
+TargetLatency target_latency(int64_t wait_count, const SLOSpec& slo, const TradeoffModel& tm,
+                             double q_ref);
+int64_t binary_search_budget(int64_t b, double target_ms, const PerfParams& params,
+                             const SchedulerConfig& cfg, int64_t s_cap = -1);
+std::vector<Allocation> allocate_tokens(std::span<const Request* const> run_q,
+                                        std::span<const Request* const> wait_q, int64_t b, int64_t s);
+BatchPlan schedule_step(std::span<const Request* const> wait_q, std::span<const Request* const> run_q,
+                        const SLOSpec& slo, const TradeoffModel& tm, const PerfParams& params,
+                        const SchedulerConfig& cfg);
+
+struct CompletionStats {
+  double ttft_ms = 0.0;
+  double tpot_ms = 0.0;
+  int64_t decode_len = 0;
+};
+
+class TradeoffEstimator {
+ public:
+  explicit TradeoffEstimator(const TradeoffModel& initial);
+  void update(std::span<const CompletionStats> completed);
+  const TradeoffModel& model() const { return model_; }
+  int64_t degenerate_updates() const { return degenerate_updates_; }
+
+ private:
+  TradeoffModel model_;
+  std::vector<double> win_ttft_, win_tpot_;  // device-layout ring (NX_TRADEOFF_WINDOW)
+  int32_t win_head_ = 0, win_len_ = 0;
+  int64_t degenerate_updates_ = 0;
+};
+
+// ---- router (router.h) ----------------------------------------------------------
+enum class RouterPolicy { kPrism, kRoundRobin, kSessionAffinity, kLeastLoaded, kLatencyBased, kWeighted };
+
+RouterPolicy router_policy_from_string(const std::string& name);
+std::string to_string(RouterPolicy policy);
+
+struct RouterConfig {
+  RouterPolicy policy = RouterPolicy::kPrism;
+  std::array<double, 4> weights{1.0, 1.0, 1.0, 1.0};
+  double beta_aff = 1.5;
+  double latency_knee = 0.5;
+  double latency_scale_ms = 0.0;
+  double load_half_ms = 50.0;
+  double capacity_headroom = 2.0;
+  double staleness_limit_ms = 1000.0;
+  double latency_window_ms = 2000.0;
+  std::map<int, double> static_weights;
+  bool valid() const {
+    bool w_ok = true;
+    for (double w : weights) w_ok = w_ok && w >= 0.0;
+    return w_ok && beta_aff > 1.0 && latency_knee >= 0.0 && latency_scale_ms >= 0.0 &&
+           load_half_ms > 0.0 && capacity_headroom >= 1.0 && staleness_limit_ms > 0.0 &&
+           latency_window_ms > 0.0;
+  }
+};
+
+double score_latency(const StateVector& sv, const SLOSpec& slo, const RouterConfig& cfg);
+double score_load(const StateVector& sv, const RouterConfig& cfg);
+double score_capacity(const StateVector& sv, double req_demand_tokens, const RouterConfig& cfg);
+
+struct RouteDecision {
+  int engine_id = -1;
+  double score = 0.0;
+  std::array<double, 4> factors{1.0, 1.0, 1.0, 1.0};
+  bool degraded = false;
+};
+
+class Router {
+ public:
+  Router(const RouterConfig& cfg, const SLOSpec& slo, uint64_t root_seed);
+  void register_engine(int engine_id);
+  void on_report(const EngineReport& report);
+  void on_completion(int engine_id, const std::string& session_id, double e2e_ms,
+                     int64_t decode_len, double now_ms);
+  RouteDecision route(const Request& request, double now_ms);
+  double score_affinity(int engine_id, const std::string& session_id) const;
+  double demand_estimate_tokens(int64_t prompt_len) const;
+  size_t engine_count() const { return order_.size(); }
+
+ private:
+  struct EngineInfo {
+    std::optional<EngineReport> report;
+    std::deque<std::pair<double, double>> latencies;
+    double latency_sum = 0.0;
+  };
+  void remember_session(const std::string& session_id, int engine_id);
+  RouterConfig cfg_;
+  SLOSpec slo_;
+  std::array<uint64_t, 4> rng_{};
+  uint64_t rr_next_ = 0;
+  std::vector<int> order_;
+  std::unordered_map<int, EngineInfo> engines_;
+  std::unordered_map<std::string, int> sessions_;  // session -> engine id
+  std::deque<std::string> session_lru_;
+  double l_bar_ema_ = 128.0;
+};
+
+// ---- online learner (learner.h) ------------------------------------------------------
+struct LearnerConfig {
+  int64_t long_window = 4096;
+  int64_t short_window = 64;
+  int64_t structural_period = 1024;
+  int64_t linear_period = 32;
+  int64_t min_structural_samples = 256;
+  bool valid() const {
+    return long_window > 0 && short_window > 0 && structural_period > 0 && linear_period > 0 &&
+           min_structural_samples > 0 && short_window < long_window &&
+           linear_period < structural_period;
+  }
+};
+
+struct LearnerCounters {
+  int64_t linear_updates = 0;
+  int64_t structural_updates = 0;
+  int64_t degenerate_updates = 0;
+  int64_t rescale_updates = 0;
+  int64_t clamp_events = 0;
+  int64_t failed_fits = 0;
+  int64_t low_identifiability = 0;
+};
+
+class OnlineLearner {
+ public:
+  OnlineLearner(const PerfParams& priors, const LearnerConfig& cfg);
+  static PerfParams default_priors();
+  void record_sample(const LatencySample& sample);
+  const PerfParams& params() const { return current_; }
+  int64_t samples_seen() const { return samples_seen_; }
+  int64_t buffered() const { return static_cast<int64_t>(ring_.size()); }
+  const LearnerCounters& counters() const { return counters_; }
+  const LearnerConfig& config() const { return cfg_; }
+  bool update_linear();
+  bool update_structural();
+  double convergence_error(std::span<const LatencySample> probe) const;
+  std::string to_json() const;
+
+ private:
+  bool refit(int kind);
+  LearnerConfig cfg_;
+  PerfParams current_;
+  std::vector<LatencySample> ring_;
+  size_t ring_head_ = 0;
+  int64_t samples_seen_ = 0;
+  LearnerCounters counters_;
+};
+
+std::vector<LatencySample> load_samples_jsonl(const std::string& path);
+
+}  // namespace servesim

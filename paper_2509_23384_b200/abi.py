@@ -32,7 +32,7 @@ ROUTE_GROUP = np.dtype([
 ENGINE_REPORT = np.dtype([
     ("l_hat_ms", "f8"), ("w_load_tokens", "f8"), ("m_free_tokens", "f8"), ("p_max", "f8"),
     ("reported_at_ms", "f8"), ("static_weight", "f8"), ("queue_len", "i8"), ("engine_id", "i4"),
-    ("has_report", "i4")], align=True)
+    ("has_report", "i4"), ("rolling_latency_ms", "f8")], align=True)
 
 ROUTE_REQUEST = np.dtype([("now_ms", "f8"), ("prompt_len", "i8"), ("session", "i4"),
                           ("pad_", "i4")], align=True)

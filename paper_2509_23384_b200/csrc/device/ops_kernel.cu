@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(32 * kRouteWarps) nx_route_kernel(
     for (int i = 0; i < 4; ++i) cfg_ok = cfg_ok && G.weights[i] >= 0.0;
     if (n < 1) status = NX_ERUNTIME;  // route: no engines registered (router.cpp:142)
     else if (!cfg_ok || n > 32 || G.n_sessions < 0 || G.n_sessions > kSessionCapacity ||
-             !(pol == 0 || pol == 1 || pol == 2 || pol == 3 || pol == 5))
+             !(pol >= 0 && pol <= 5) || (pol == 4 && G.n_requests > 1))
       status = NX_EINVAL;
     if (status != NX_OK) {
       if (lane == 0) gstatus[gi] = status;
@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(32 * kRouteWarps) nx_route_kernel(
     v.qlen = 0;
     v.id = 0x7fffffff;
     v.affine = false;
-    double sw = 0.0;
+    double sw = 0.0, lat = 0.0;
     if (v.on) {
       const nx_engine_report& r = rows[lane];
       v.has_rep = r.has_report != 0;
@@ -167,6 +167,7 @@ __global__ void __launch_bounds__(32 * kRouteWarps) nx_route_kernel(
       v.qlen = r.queue_len;
       v.id = r.engine_id;
       sw = r.static_weight;
+      lat = r.rolling_latency_ms;
     }
     RouterCfgD rc;
     for (int i = 0; i < 4; ++i) rc.w[i] = G.weights[i];
@@ -211,6 +212,18 @@ __global__ void __launch_bounds__(32 * kRouteWarps) nx_route_kernel(
         case 3:  // least_loaded (:157-170)
           chosen = prism_least_loaded(v);
           break;
+        case 4: {  // latency_based (:172-184): first strict minimum, NaN never wins
+          double best = __builtin_huge_val();
+          chosen = 0;
+          for (int e = 0; e < n; ++e) {
+            const double l = __shfl_sync(NX_FULL, lat, e);
+            if (l < best) {
+              best = l;
+              chosen = e;
+            }
+          }
+          break;
+        }
         case 5: {  // weighted draw (:186-203), sequential over lanes on every lane
           double total = 0.0;
           for (int e = 0; e < n; ++e) total += __shfl_sync(NX_FULL, sw, e);

@@ -101,6 +101,50 @@ struct Arena {
 
 constexpr int kWarpsPerBlock = 2;  // event-loop warp + refit warp per replica CTA
 
+
+int current_sms() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return sm_count(dev);
+}
+
+// Device staging for the host-pointer entry points: one grow-only buffer per
+// thread and device, so a scalar call (the C++ drop-in's predict_latency,
+// route, ...) costs copies + one launch, not a cudaMalloc.
+struct Staging {
+  Arena A;
+  unsigned char* d = nullptr;
+  void alloc() {
+    struct Buf {
+      unsigned char* p = nullptr;
+      size_t cap = 0;
+      int dev = -1;
+    };
+    thread_local Buf buf;
+    int dev = 0;
+    cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+    if (buf.dev != dev || buf.cap < A.size) {
+      if (buf.p && buf.dev == dev) cudaFree(buf.p);
+      buf.cap = std::max<size_t>(A.size, size_t(1) << 20);
+      cuda_check(cudaMalloc(&buf.p, buf.cap), "cudaMalloc");
+      buf.dev = dev;
+    }
+    d = buf.p;
+  }
+  template <class T>
+  T* at(size_t off) { return reinterpret_cast<T*>(d + off); }
+};
+
+const char* status_text(int st) {
+  switch (st) {
+    case NX_EINVAL: return "invalid argument";
+    case NX_ERUNTIME: return "runtime error";
+    case NX_ELOGIC: return "logic error";
+  }
+  return "error";
+}
+
+
 }  // namespace
 
 struct nx_sim {
@@ -735,13 +779,13 @@ int nx_perf_eval_host(const double* params, int32_t n_params, const int32_t* idx
                       const int32_t* s, double* out_T, double* out_thr, int64_t n, int32_t mode) {
   return guard([&] {
     if (n < 0 || n_params < 1) throw std::invalid_argument("nx_perf_eval: empty parameter table");
-    unsigned char* d = nullptr;
-    Arena A;
+    Staging S;
+    Arena& A = S.A;
     const size_t op = A.take<double>(8 * static_cast<size_t>(n_params));
     const size_t oi = A.take<int32_t>(n), ob = A.take<int32_t>(n), os = A.take<int32_t>(n);
     const size_t oT = A.take<double>(n), oh = A.take<double>(n);
-    cuda_check(cudaMalloc(&d, A.size), "cudaMalloc");
-    std::unique_ptr<unsigned char, void (*)(unsigned char*)> hold(d, [](unsigned char* p) { cudaFree(p); });
+    S.alloc();
+    unsigned char* d = S.d;
     cuda_check(cudaMemcpy(d + op, params, 8 * sizeof(double) * n_params, cudaMemcpyHostToDevice), "H2D");
     cuda_check(cudaMemcpy(d + oi, idx, sizeof(int32_t) * n, cudaMemcpyHostToDevice), "H2D");
     cuda_check(cudaMemcpy(d + ob, b, sizeof(int32_t) * n, cudaMemcpyHostToDevice), "H2D");
@@ -760,34 +804,6 @@ int nx_perf_eval_host(const double* params, int32_t n_params, const int32_t* idx
 }  // extern "C"
 
 namespace {
-
-int current_sms() {
-  int dev = 0;
-  cudaGetDevice(&dev);
-  return sm_count(dev);
-}
-
-// Device copy of a host array inside an arena; returns the offset.
-struct Staging {
-  Arena A;
-  unsigned char* d = nullptr;
-  void alloc() { cuda_check(cudaMalloc(&d, A.size), "cudaMalloc"); }
-  ~Staging() {
-    if (d) cudaFree(d);
-  }
-  template <class T>
-  T* at(size_t off) { return reinterpret_cast<T*>(d + off); }
-};
-
-const char* status_text(int st) {
-  switch (st) {
-    case NX_EINVAL: return "invalid argument";
-    case NX_ERUNTIME: return "runtime error";
-    case NX_ELOGIC: return "logic error";
-  }
-  return "error";
-}
-
 }  // namespace
 
 extern "C" {

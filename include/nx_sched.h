@@ -312,6 +312,37 @@ int nx_sim_phase_cycles(nx_sim_t h, int32_t replica, int64_t* out10);
 /* %globaltimer (ns) at which the replica's CTA started and finished it
  * (diagnostic: per-replica latency under co-residency). */
 int nx_sim_timeline(nx_sim_t h, int32_t replica, int64_t* begin_end_ns);
+/* ---- observability (RunConfig.output / record_learner_history) ------------
+ * Written by the device during the run when the config asks for them
+ * (output.plans_jsonl, output.routing_jsonl, record_learner_history):
+ * one plan row per started step (sim.cpp:149-158), one routing row per
+ * arrival (sim.cpp:176-186), one learner snapshot per learner update event
+ * (sim.cpp:322-327). */
+typedef struct nx_plan_log_row {
+  double sim_time_ms;
+  int32_t engine_id, pad_;
+  int64_t b, s;
+  double predicted_ms, target_ms;
+} nx_plan_log_row;
+typedef struct nx_route_log_row {
+  double sim_time_ms;
+  int64_t request_id;
+  int32_t chosen_engine, pad_;
+  double s_latency, s_load, s_capacity, s_affinity, score;
+} nx_route_log_row;
+typedef struct nx_learner_snapshot {  /* LearnerSnapshot (sim.h:62-67) */
+  int32_t engine_id, pad_;
+  double sim_time_ms;
+  int64_t samples_seen;
+  double params[8];
+} nx_learner_snapshot;
+int nx_sim_plan_log(nx_sim_t h, int32_t replica, nx_plan_log_row* out, int64_t cap, int64_t* n);
+int nx_sim_route_log(nx_sim_t h, int32_t replica, nx_route_log_row* out, int64_t cap, int64_t* n);
+int nx_sim_learner_history(nx_sim_t h, int32_t replica, nx_learner_snapshot* out, int64_t cap,
+                           int64_t* n);
+/* Simulation::write_outputs (sim.cpp:393-413): summary.json, requests.csv and
+ * the JSONL logs into the config's output.dir (no-op when it is empty). */
+int nx_sim_write_outputs(nx_sim_t h, int32_t replica);
 /* Learner state per engine: params[8] + samples + counters[7]. */
 int nx_sim_learner(nx_sim_t h, int32_t replica, int32_t engine, double* params8,
                    int64_t* samples, int64_t* counters7);

@@ -122,6 +122,15 @@ int ref_run_json(const char* cfg_json, int with_records, char** out) {
       j["rec_first"] = ft;
       j["rec_done"] = done;
     }
+    if (cfg.record_learner_history) {  // RunResult::learner_history (sim.cpp:322-327)
+      nlohmann::ordered_json hist = nlohmann::ordered_json::array();
+      for (const auto& h : r.learner_history) {
+        double p8[8];
+        params_to(h.params, p8);
+        hist.push_back({h.engine_id, h.sim_time_ms, h.samples_seen, std::vector<double>(p8, p8 + 8)});
+      }
+      j["learner_history"] = hist;
+    }
     *out = dup_string(j.dump());
     return 0;
   } catch (const std::exception& e) {

@@ -38,6 +38,23 @@ class RequestRecord(C.Structure):
                 ("engine_id", C.c_int32), ("pad_", C.c_int32)]
 
 
+class PlanLogRow(C.Structure):
+    _fields_ = [("sim_time_ms", C.c_double), ("engine_id", C.c_int32), ("pad_", C.c_int32),
+                ("b", C.c_int64), ("s", C.c_int64), ("predicted_ms", C.c_double),
+                ("target_ms", C.c_double)]
+
+
+class RouteLogRow(C.Structure):
+    _fields_ = [("sim_time_ms", C.c_double), ("request_id", C.c_int64), ("chosen_engine", C.c_int32),
+                ("pad_", C.c_int32), ("s_latency", C.c_double), ("s_load", C.c_double),
+                ("s_capacity", C.c_double), ("s_affinity", C.c_double), ("score", C.c_double)]
+
+
+class LearnerSnapshot(C.Structure):
+    _fields_ = [("engine_id", C.c_int32), ("pad_", C.c_int32), ("sim_time_ms", C.c_double),
+                ("samples_seen", C.c_int64), ("params", C.c_double * 8)]
+
+
 _lib = None
 _P = C.POINTER
 
@@ -81,6 +98,10 @@ def lib() -> C.CDLL:
     L.nx_synth_generate.argtypes = [C.c_char_p, C.c_int64, C.c_uint64, _P(C.c_int64),
                                     _P(C.c_int64), C.c_char_p]
     V = C.c_void_p
+    for fn, row in (("nx_sim_plan_log", PlanLogRow), ("nx_sim_route_log", RouteLogRow),
+                    ("nx_sim_learner_history", LearnerSnapshot)):
+        getattr(L, fn).argtypes = [C.c_void_p, C.c_int32, _P(row), C.c_int64, _P(C.c_int64)]
+    L.nx_sim_write_outputs.argtypes = [C.c_void_p, C.c_int32]
     L.nx_rng_state.argtypes = [C.c_uint64, C.c_char_p, C.c_uint64, _P(C.c_uint64)]
     L.nx_abi_sizes.argtypes = [_P(C.c_int64), C.c_int32]
     L.nx_lens_schedule_dev.argtypes = [V, C.c_int32, V, C.c_int64, V, V, V]

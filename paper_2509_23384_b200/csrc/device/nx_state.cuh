@@ -60,6 +60,7 @@ struct RepSm {
   int64_t work[6];
   int64_t cycles[16];
   int64_t t_begin_ns;
+  int64_t n_plan_log, n_route_log, n_learn_log;
   double l_bar_ema;
   uint32_t next_seq;
   int32_t cursor, status, site;

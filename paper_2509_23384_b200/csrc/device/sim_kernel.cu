@@ -284,7 +284,9 @@ __device__ NX_COLD void try_begin_step(Ctx& c, int e, int64_t now_us) {
       g.memo_truth = truth;
     }
     write_decodes(c, c.P->rq + ed.rq_off, R, c.P->plan_req + ed.plan_off, c.P->plan_tok + ed.plan_off);
-    set_plan(c, g, R, R, R, pred, 0.0, 0, 0, R);
+    // BatchPlan::target_ms = target_latency(0 waiters) (lens.cpp:103-104);
+    // validated configs make it positive (tpot, td_min > 0)
+    set_plan(c, g, R, R, R, pred, target_latency(c, g, 0), 0, 0, R);
   } else {
     if (ed.policy == 0) plan_lens(c, e);
     else plan_baseline(c, e);
@@ -306,6 +308,23 @@ __device__ NX_COLD void try_begin_step(Ctx& c, int e, int64_t now_us) {
     g.step_seq = c.rs->next_seq++;
     c.rs->work[0] += 1;
     c.rs->work[1] += g.plan_b;
+    if (c.d->log_flags & NX_LOG_PLANS) {  // plans_jsonl row (sim.cpp:149-158)
+      const int64_t k = c.rs->n_plan_log;
+      if (k >= c.d->plan_log_cap) {
+        c.rs->status = 1;
+        c.rs->site = NX_SITE_OVERFLOW;
+      } else {
+        NxPlanLog& L = c.P->plan_log[c.d->plan_log_off + k];
+        L.t_us = now_us;
+        L.engine_id = ed.engine_id;
+        L.b = g.plan_b;
+        L.s = g.plan_s;
+        L.pad_ = 0;
+        L.predicted_ms = g.plan_pred;
+        L.target_ms = g.plan_target;
+        c.rs->n_plan_log = k + 1;
+      }
+    }
   }
   __syncwarp();
 }
@@ -679,7 +698,7 @@ __device__ int least_loaded(Ctx& c) {
   return warp_argmin_i64(len, on);
 }
 
-__device__ NX_COLD int route(Ctx& c, int rid, double now) {
+__device__ NX_COLD int route(Ctx& c, int rid, double now, double& score, double (&fac)[4]) {
   const NxReplicaDesc& d = *c.d;
   const int n = c.n_eng;
   const int sess = c.P->session[c.roff + rid];
@@ -798,7 +817,10 @@ __device__ NX_COLD int route(Ctx& c, int rid, double now) {
       rc.headroom = d.headroom;
       rc.stale_limit = d.stale_limit;
       rc.ttft_slo = d.ttft_slo;
-      chosen = prism_choose(rc, v, demand, now, n).who;
+      const PrismPick pk = prism_choose(rc, v, demand, now, n);
+      chosen = pk.who;
+      score = pk.score;
+      for (int i = 0; i < 4; ++i) fac[i] = pk.f[i];
       __syncwarp();
       if (c.lane == 0) {  // dispatch echo (router.cpp:275-282)
         EngSm& g = c.eng[chosen];
@@ -815,6 +837,32 @@ __device__ NX_COLD int route(Ctx& c, int rid, double now) {
   if (c.lane == 0) sess_eng[sess] = chosen;  // remember_session (router.cpp:107-122)
   __syncwarp();
   return chosen;
+}
+
+// LearnerSnapshot after a learner update event (sim.cpp:322-327): the
+// structural refit record_sample may have queued is part of the update, so
+// the snapshot waits for it (history recording trades overlap for order).
+__device__ void log_learner(Ctx& c, int e, int64_t now_us) {
+  if (!(c.d->log_flags & NX_LOG_LEARNER) || failed(c)) return;
+  wait_refit(c, e);
+  __syncwarp();
+  if (c.lane == 0) {
+    const int64_t k = c.rs->n_learn_log;
+    if (k >= c.d->learn_log_cap) {
+      c.rs->status = 1;
+      c.rs->site = NX_SITE_OVERFLOW;
+    } else {
+      const EngSm& g = c.eng[e];
+      NxLearnLog& L = c.P->learn_log[c.d->learn_log_off + k];
+      L.t_us = now_us;
+      L.samples = g.seen;
+      L.engine_id = c.ed[e].engine_id;
+      L.pad_ = 0;
+      params_to(g.lp, L.params);
+      c.rs->n_learn_log = k + 1;
+    }
+  }
+  __syncwarp();
 }
 
 // ---- replica driver -------------------------------------------------------------
@@ -853,6 +901,9 @@ __device__ NX_COLD void init_replica(Ctx& c) {
     for (int i = 0; i < 6; ++i) R.work[i] = 0;
     for (int i = 0; i < 16; ++i) R.cycles[i] = 0;
     R.t_begin_ns = nx_globaltimer();
+    R.n_plan_log = 0;
+    R.n_route_log = 0;
+    R.n_learn_log = 0;
     R.jq_head = 0;
     R.jq_tail = 0;
     R.l_bar_ema = 128.0;
@@ -959,7 +1010,17 @@ __device__ void run_replica(Ctx& c) {
         int e, ok = 0;
         {
           PhaseTimer pt(c.rs, 1);
-          e = route(c, rid, to_ms(now));
+          double score = 0.0, fac[4] = {1.0, 1.0, 1.0, 1.0};
+          e = route(c, rid, to_ms(now), score, fac);
+          if (c.lane == 0 && (c.d->log_flags & NX_LOG_ROUTES)) {  // routing_jsonl row (sim.cpp:176-186)
+            NxRouteLog& L = c.P->route_log[c.d->route_log_off + c.rs->n_route_log];
+            L.t_us = now;
+            L.request = rid;
+            L.engine_id = c.ed[e].engine_id;
+            L.score = score;
+            for (int i = 0; i < 4; ++i) L.factors[i] = fac[i];
+            c.rs->n_route_log += 1;
+          }
           if (c.lane == 0 && !failed(c)) {
             ok = admit(c, e, rid) ? 1 : 0;
             if (!ok) c.rs->rejected += 1;
@@ -995,6 +1056,7 @@ __device__ void run_replica(Ctx& c) {
         __syncwarp();
         const EngSm& g = c.eng[who];
         record_sample(c, who, g.learn_b, g.learn_s, g.learn_y);
+        log_learner(c, who, now);
         break;
       }
       case 2: {
@@ -1005,6 +1067,7 @@ __device__ void run_replica(Ctx& c) {
       case 3: {
         const EngSm& g = c.eng[who];
         record_sample(c, who, g.learn_b, g.learn_s, g.learn_y);
+        log_learner(c, who, now);
         break;
       }
       case 4: {  // report delivery -> Router::on_report (router.cpp:75-81)
@@ -1044,6 +1107,9 @@ __device__ NX_COLD void write_outputs(Ctx& c, int r) {
     for (int i = 0; i < 6; ++i) o.work[i] = R.work[i];
     for (int i = 0; i < 16; ++i) o.cycles[i] = R.cycles[i];
     o.t_begin_ns = R.t_begin_ns;
+    o.n_plan_log = R.n_plan_log;
+    o.n_route_log = R.n_route_log;
+    o.n_learn_log = R.n_learn_log;
     o.t_end_ns = nx_globaltimer();
   }
   for (int e = c.lane; e < c.n_eng; e += 32) {

@@ -10,6 +10,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <filesystem>
+#include <fstream>
 #include <memory>
 #include <numeric>
 #include <stdexcept>
@@ -20,6 +22,7 @@
 #include "../nx_layout.h"
 #include "frontend.hpp"
 #include "nx_sched.h"
+#include "json.hpp"
 #include "report.hpp"
 
 extern "C" cudaError_t nx_launch_sim(const NxPools* d_pools, const int32_t* d_order, int n_rep,
@@ -171,6 +174,11 @@ struct nx_sim {
   int64_t* h_first_us = nullptr;
   int64_t* h_done_us = nullptr;
   int32_t* h_req_engine = nullptr;
+  // observability logs (allocated only when a replica asks for them)
+  int64_t n_plan_log = 0, n_route_log = 0, n_learn_log = 0;
+  NxPlanLog* h_plan_log = nullptr;
+  NxRouteLog* h_route_log = nullptr;
+  NxLearnLog* h_learn_log = nullptr;
   // device
   unsigned char* d_arena = nullptr;
   size_t arena_bytes = 0;
@@ -190,7 +198,8 @@ struct nx_sim {
     if (d_pools) cudaFree(d_pools);
     for (void* p : {(void*)h_arr_us, (void*)h_arr_ms, (void*)h_prompt, (void*)h_target,
                     (void*)h_session, (void*)h_rep_out, (void*)h_eng_out, (void*)h_records,
-                    (void*)h_first_us, (void*)h_done_us, (void*)h_req_engine})
+                    (void*)h_first_us, (void*)h_done_us, (void*)h_req_engine, (void*)h_plan_log,
+                    (void*)h_route_log, (void*)h_learn_log})
       if (p) cudaFreeHost(p);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
@@ -254,6 +263,21 @@ void fill_descriptors(nx_sim& h) {
     d.s_period = static_cast<int32_t>(c.structural_period);
     d.l_period = static_cast<int32_t>(c.linear_period);
     d.min_s = static_cast<int32_t>(std::min<int64_t>(c.min_structural, INT32_MAX));
+    // observability: plans / learner snapshots are one per executed step, and
+    // every step advances at least one token of some request
+    d.log_flags = (c.out_plans_jsonl.empty() ? 0 : NX_LOG_PLANS) |
+                  (c.out_routing_jsonl.empty() ? 0 : NX_LOG_ROUTES) |
+                  (c.record_learner_history ? NX_LOG_LEARNER : 0);
+    int64_t token_bound = 16;
+    for (int i = 0; i < n; ++i) token_bound += static_cast<int64_t>(w.prompt[i]) + w.output[i];
+    d.plan_log_off = h.n_plan_log;
+    d.plan_log_cap = (d.log_flags & NX_LOG_PLANS) ? token_bound : 0;
+    h.n_plan_log += d.plan_log_cap;
+    d.route_log_off = h.n_route_log;
+    h.n_route_log += (d.log_flags & NX_LOG_ROUTES) ? n : 0;
+    d.learn_log_off = h.n_learn_log;
+    d.learn_log_cap = (d.log_flags & NX_LOG_LEARNER) ? token_bound : 0;
+    h.n_learn_log += d.learn_log_cap;
     req_off += n;
     sess_off += ns;
     scratch_off += (10 * static_cast<int64_t>(c.long_window) + 1024 + 5120 + 64 + 31) / 32 * 32;  // nx_learner.cuh layout
@@ -353,6 +377,9 @@ void fill_descriptors(nx_sim& h) {
   const size_t o_late = A.take<double>(lat_off);
   const size_t o_rec = A.take<int32_t>(h.n_req);
   const size_t o_scr = A.take<double>(scratch_off);
+  const size_t o_plog = A.take<NxPlanLog>(h.n_plan_log);
+  const size_t o_rlog = A.take<NxRouteLog>(h.n_route_log);
+  const size_t o_llog = A.take<NxLearnLog>(h.n_learn_log);
   h.off_rep_out = A.take<NxReplicaOut>(h.n_rep);
   h.off_eng_out = A.take<NxEngineOut>(h.n_eng);
   h.arena_bytes = A.size;
@@ -392,6 +419,9 @@ void fill_descriptors(nx_sim& h) {
   P.sess_engine = reinterpret_cast<int32_t*>(B + o_sess_eng);
   P.records = reinterpret_cast<int32_t*>(B + o_rec);
   P.scratch = reinterpret_cast<double*>(B + o_scr);
+  P.plan_log = reinterpret_cast<NxPlanLog*>(B + o_plog);
+  P.route_log = reinterpret_cast<NxRouteLog*>(B + o_rlog);
+  P.learn_log = reinterpret_cast<NxLearnLog*>(B + o_llog);
   P.rep = reinterpret_cast<const NxReplicaDesc*>(B + h.off_rep);
   P.eng = reinterpret_cast<const NxEngineDesc*>(B + h.off_eng);
   P.rep_out = reinterpret_cast<NxReplicaOut*>(B + h.off_rep_out);
@@ -434,6 +464,9 @@ void fill_descriptors(nx_sim& h) {
   h.h_first_us = pinned<int64_t>(h.n_req);
   h.h_done_us = pinned<int64_t>(h.n_req);
   h.h_req_engine = pinned<int32_t>(h.n_req);
+  if (h.n_plan_log) h.h_plan_log = pinned<NxPlanLog>(h.n_plan_log);
+  if (h.n_route_log) h.h_route_log = pinned<NxRouteLog>(h.n_route_log);
+  if (h.n_learn_log) h.h_learn_log = pinned<NxLearnLog>(h.n_learn_log);
 }
 
 const char* site_name(int site) {
@@ -563,6 +596,9 @@ int nx_sim_download(nx_sim_t h) {
     cp(h->h_first_us, P.first_us, h->n_req * sizeof(int64_t));
     cp(h->h_done_us, P.done_us, h->n_req * sizeof(int64_t));
     cp(h->h_req_engine, P.req_engine, h->n_req * sizeof(int32_t));
+    if (h->n_plan_log) cp(h->h_plan_log, P.plan_log, h->n_plan_log * sizeof(NxPlanLog));
+    if (h->n_route_log) cp(h->h_route_log, P.route_log, h->n_route_log * sizeof(NxRouteLog));
+    if (h->n_learn_log) cp(h->h_learn_log, P.learn_log, h->n_learn_log * sizeof(NxLearnLog));
   });
 }
 
@@ -682,6 +718,121 @@ int nx_sim_summary_json(nx_sim_t h, int32_t replica, char* buf, int64_t cap, int
       const size_t k = std::min<size_t>(s.size(), static_cast<size_t>(cap - 1));
       std::memcpy(buf, s.data(), k);
       buf[k] = 0;
+    }
+  });
+}
+
+int nx_sim_plan_log(nx_sim_t h, int32_t replica, nx_plan_log_row* out, int64_t cap, int64_t* n) {
+  return guard([&] {
+    if (replica < 0 || replica >= h->n_rep) throw std::invalid_argument("replica out of range");
+    const NxReplicaDesc& d = h->rep[replica];
+    const int64_t m = (d.log_flags & NX_LOG_PLANS) ? h->h_rep_out[replica].n_plan_log : 0;
+    *n = m;
+    for (int64_t k = 0; k < std::min(cap, m); ++k) {
+      const NxPlanLog& L = h->h_plan_log[d.plan_log_off + k];
+      out[k] = {nx::to_ms(L.t_us), L.engine_id, 0, L.b, L.s, L.predicted_ms, L.target_ms};
+    }
+  });
+}
+
+int nx_sim_route_log(nx_sim_t h, int32_t replica, nx_route_log_row* out, int64_t cap, int64_t* n) {
+  return guard([&] {
+    if (replica < 0 || replica >= h->n_rep) throw std::invalid_argument("replica out of range");
+    const NxReplicaDesc& d = h->rep[replica];
+    const int64_t m = (d.log_flags & NX_LOG_ROUTES) ? h->h_rep_out[replica].n_route_log : 0;
+    *n = m;
+    for (int64_t k = 0; k < std::min(cap, m); ++k) {
+      const NxRouteLog& L = h->h_route_log[d.route_log_off + k];
+      out[k] = {nx::to_ms(L.t_us), L.request, L.engine_id, 0, L.factors[0], L.factors[1],
+                L.factors[2], L.factors[3], L.score};
+    }
+  });
+}
+
+int nx_sim_learner_history(nx_sim_t h, int32_t replica, nx_learner_snapshot* out, int64_t cap,
+                           int64_t* n) {
+  return guard([&] {
+    if (replica < 0 || replica >= h->n_rep) throw std::invalid_argument("replica out of range");
+    const NxReplicaDesc& d = h->rep[replica];
+    const int64_t m = (d.log_flags & NX_LOG_LEARNER) ? h->h_rep_out[replica].n_learn_log : 0;
+    *n = m;
+    for (int64_t k = 0; k < std::min(cap, m); ++k) {
+      const NxLearnLog& L = h->h_learn_log[d.learn_log_off + k];
+      nx_learner_snapshot& o = out[k];
+      o.engine_id = L.engine_id;
+      o.pad_ = 0;
+      o.sim_time_ms = nx::to_ms(L.t_us);
+      o.samples_seen = L.samples;
+      for (int i = 0; i < 8; ++i) o.params[i] = L.params[i];
+    }
+  });
+}
+
+// Simulation::write_outputs (sim.cpp:393-413): summary.json, requests.csv and
+// the two JSONL logs (rows as sim.cpp:149-158, 176-186 format them).
+int nx_sim_write_outputs(nx_sim_t h, int32_t replica) {
+  return guard([&] {
+    if (replica < 0 || replica >= h->n_rep) throw std::invalid_argument("replica out of range");
+    const nx::RunCfg& c = h->cfgs[replica];
+    if (c.out_dir.empty()) return;
+    namespace fs = std::filesystem;
+    const fs::path dir(c.out_dir);
+    fs::create_directories(dir);
+    if (!c.out_summary.empty()) {
+      int64_t len = 0;
+      if (nx_sim_summary_json(h, replica, nullptr, 0, &len) != NX_OK) throw std::runtime_error(g_err);
+      std::string s(static_cast<size_t>(len) + 1, '\0');
+      nx_sim_summary_json(h, replica, s.data(), len + 1, &len);
+      s.resize(static_cast<size_t>(len));
+      std::ofstream out(dir / c.out_summary);
+      out << s;
+    }
+    if (!c.out_requests_csv.empty()) {
+      const NxReplicaOut& o = h->h_rep_out[replica];
+      std::vector<nx_request_record> recs(static_cast<size_t>(o.completed));
+      int64_t n = 0;
+      if (nx_sim_records(h, replica, recs.data(), o.completed, &n) != NX_OK) throw std::runtime_error(g_err);
+      std::vector<nx::RecordRow> rows(recs.size());
+      for (size_t i = 0; i < recs.size(); ++i)
+        rows[i] = {recs[i].request_id, recs[i].arrival_ms, recs[i].first_token_ms, recs[i].completed_ms,
+                   recs[i].prompt_tokens, recs[i].output_tokens, recs[i].engine_id};
+      nx::write_requests_csv((dir / c.out_requests_csv).string(), rows);
+    }
+    if (!c.out_plans_jsonl.empty()) {
+      int64_t n = 0;
+      nx_sim_plan_log(h, replica, nullptr, 0, &n);
+      std::vector<nx_plan_log_row> rows(static_cast<size_t>(n));
+      nx_sim_plan_log(h, replica, rows.data(), n, &n);
+      std::ofstream out(dir / c.out_plans_jsonl);
+      for (const auto& r : rows) {
+        nlohmann::ordered_json j;
+        j["sim_time"] = r.sim_time_ms;
+        j["engine_id"] = r.engine_id;
+        j["b"] = r.b;
+        j["s"] = r.s;
+        j["predicted_ms"] = r.predicted_ms;
+        j["target_ms"] = r.target_ms;
+        out << j.dump() << '\n';
+      }
+    }
+    if (!c.out_routing_jsonl.empty()) {
+      int64_t n = 0;
+      nx_sim_route_log(h, replica, nullptr, 0, &n);
+      std::vector<nx_route_log_row> rows(static_cast<size_t>(n));
+      nx_sim_route_log(h, replica, rows.data(), n, &n);
+      std::ofstream out(dir / c.out_routing_jsonl);
+      for (const auto& r : rows) {
+        nlohmann::ordered_json j;
+        j["sim_time"] = r.sim_time_ms;
+        j["request_id"] = static_cast<uint64_t>(r.request_id);
+        j["chosen_engine"] = r.chosen_engine;
+        j["s_latency"] = r.s_latency;
+        j["s_load"] = r.s_load;
+        j["s_capacity"] = r.s_capacity;
+        j["s_affinity"] = r.s_affinity;
+        j["score"] = r.score;
+        out << j.dump() << '\n';
+      }
     }
   });
 }

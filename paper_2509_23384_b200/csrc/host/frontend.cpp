@@ -243,6 +243,15 @@ RunCfg parse_run_config(const std::string& text) {
     c.time_scale = opt<double>(w, "time_scale", c.time_scale);
     c.poisson = opt<bool>(w, "poisson", c.poisson);
   }
+  c.record_learner_history = opt<bool>(j, "record_learner_history", c.record_learner_history);
+  if (j.contains("output")) {  // OutputConfig (sim.cpp:570-579)
+    const auto& o = j["output"];
+    c.out_dir = opt<std::string>(o, "dir", c.out_dir);
+    c.out_summary = opt<std::string>(o, "summary", c.out_summary);
+    c.out_requests_csv = opt<std::string>(o, "requests_csv", c.out_requests_csv);
+    c.out_plans_jsonl = opt<std::string>(o, "plans_jsonl", c.out_plans_jsonl);
+    c.out_routing_jsonl = opt<std::string>(o, "routing_jsonl", c.out_routing_jsonl);
+  }
   validate_run_config(c);
   return c;
 }

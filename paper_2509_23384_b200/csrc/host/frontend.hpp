@@ -108,6 +108,10 @@ struct RunCfg {
   int64_t n = 100;
   double time_scale = 1.0;
   bool poisson = false;
+  // observability (RunConfig::record_learner_history, OutputConfig; sim.h)
+  bool record_learner_history = false;
+  std::string out_dir, out_summary = "summary.json", out_requests_csv = "requests.csv";
+  std::string out_plans_jsonl, out_routing_jsonl;
 };
 
 // Throws std::runtime_error / std::invalid_argument with the reference's

@@ -44,8 +44,29 @@ typedef struct NxReplicaDesc {
   int32_t n_eng, eng_base, n_req, n_sess;
   int32_t n_iters, route_policy;
   int32_t long_w, short_w, s_period, l_period, min_s;
-  int32_t pad_;
+  int32_t log_flags;       /* NX_LOG_* observability streams of this replica */
+  int64_t plan_log_off, route_log_off, learn_log_off;  /* record offsets in the log pools */
+  int64_t plan_log_cap, learn_log_cap;                 /* capacities (route log: n_req) */
 } NxReplicaDesc;
+
+/* Observability streams (proj/src/sim.cpp:149-158, 176-186, 322-327): written
+   by the device as the events happen, formatted on the host. */
+enum { NX_LOG_PLANS = 1, NX_LOG_ROUTES = 2, NX_LOG_LEARNER = 4 };
+typedef struct NxPlanLog {   /* plans_jsonl row: the inflight plan of a started step */
+  int64_t t_us;
+  int32_t engine_id, b, s, pad_;
+  double predicted_ms, target_ms;
+} NxPlanLog;
+typedef struct NxRouteLog {  /* routing_jsonl row: one RouteDecision */
+  int64_t t_us;
+  int32_t request, engine_id;
+  double score, factors[4];
+} NxRouteLog;
+typedef struct NxLearnLog {  /* LearnerSnapshot after a learner update event */
+  int64_t t_us, samples;
+  int32_t engine_id, pad_;
+  double params[8];
+} NxLearnLog;
 
 /* Per-replica result (device -> host). */
 typedef struct NxReplicaOut {
@@ -67,6 +88,7 @@ typedef struct NxReplicaOut {
   int64_t cycles[16];
   /* %globaltimer (ns) when the replica's CTA started and finished it */
   int64_t t_begin_ns, t_end_ns;
+  int64_t n_plan_log, n_route_log, n_learn_log;  /* rows written to the logs */
 } NxReplicaOut;
 
 typedef struct NxEngineOut {
@@ -95,6 +117,7 @@ typedef struct NxPools {
   int32_t* sess_engine;
   int32_t* records;
   double* scratch;
+  NxPlanLog* plan_log; NxRouteLog* route_log; NxLearnLog* learn_log;
   /* descriptors + outputs */
   const NxReplicaDesc* rep; const NxEngineDesc* eng;
   NxReplicaOut* rep_out; NxEngineOut* eng_out;

@@ -32,6 +32,7 @@ class RunResult:  # servesim::RunResult (sim.h:62-73)
     summary_json: str
     records: list = field(default_factory=list)
     learners: list = field(default_factory=list)   # (params8, samples, counters7) per engine
+    learner_history: list = field(default_factory=list)  # LearnerSnapshot rows (sim.h:62-67)
 
     @property
     def summary(self) -> dict:
@@ -130,6 +131,36 @@ class Batch:
         check(lib().nx_sim_learner(self.h, r, e, p, C.byref(s), cnt))
         return list(p), s.value, list(cnt)
 
+    def _rows(self, fn, row, r):
+        n = C.c_int64()
+        check(getattr(lib(), fn)(self.h, r, None, 0, C.byref(n)))
+        arr = (row * max(1, n.value))()
+        check(getattr(lib(), fn)(self.h, r, arr, n.value, C.byref(n)))
+        return list(arr)[: n.value]
+
+    def plan_log(self, r: int):
+        """plans_jsonl rows (sim.cpp:149-158) written by the device."""
+        return [{"sim_time": x.sim_time_ms, "engine_id": x.engine_id, "b": x.b, "s": x.s,
+                 "predicted_ms": x.predicted_ms, "target_ms": x.target_ms}
+                for x in self._rows("nx_sim_plan_log", _lib.PlanLogRow, r)]
+
+    def route_log(self, r: int):
+        """routing_jsonl rows (sim.cpp:176-186) written by the device."""
+        return [{"sim_time": x.sim_time_ms, "request_id": x.request_id, "chosen_engine": x.chosen_engine,
+                 "s_latency": x.s_latency, "s_load": x.s_load, "s_capacity": x.s_capacity,
+                 "s_affinity": x.s_affinity, "score": x.score}
+                for x in self._rows("nx_sim_route_log", _lib.RouteLogRow, r)]
+
+    def learner_history(self, r: int):
+        """RunResult::learner_history (sim.cpp:322-327): (engine_id, sim_time_ms,
+        samples_seen, params[8]) after every learner update event."""
+        return [(x.engine_id, x.sim_time_ms, x.samples_seen, list(x.params))
+                for x in self._rows("nx_sim_learner_history", _lib.LearnerSnapshot, r)]
+
+    def write_outputs(self, r: int):
+        """Simulation::write_outputs (sim.cpp:393-413) into the config's output.dir."""
+        check(lib().nx_sim_write_outputs(self.h, r))
+
     def result(self, r: int, with_records: bool = True, n_engines: int | None = None) -> RunResult:
         s = self.summaries()[r]
         if s.status != 0:
@@ -171,8 +202,16 @@ def run_replicas(cfgs, device: int = 0, with_records: bool = False):
 
 
 def run_simulation(cfg, device: int = 0) -> RunResult:
-    """servesim::run_simulation (sim.cpp:596-599) on the device."""
-    return run_replicas([cfg], device, with_records=True)[0]
+    """servesim::run_simulation (sim.cpp:596-599) on the device; writes the
+    output files when the config names an output.dir (sim.cpp:345)."""
+    b = Batch([cfg], device).run()
+    try:
+        res = b.result(0, True)
+        res.learner_history = b.learner_history(0)
+        b.write_outputs(0)
+        return res
+    finally:
+        b.close()
 
 
 def sweep(base: dict, axis: str, values, device: int = 0):

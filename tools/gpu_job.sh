@@ -1,2 +1,3 @@
 mkdir -p gpurun_out
-(time timeout 1500 ./tests/refsuite/_bin/refsuite) > gpurun_out/refsuite.txt 2>&1; echo "rc=$?" >> gpurun_out/refsuite.txt
+timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.txt 2>&1; echo "rc=$?" >> gpurun_out/pytest_gpu.txt
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.txt 2>&1; echo "rc=$?" >> gpurun_out/smoke.txt

@@ -24,6 +24,7 @@
 #include <string>
 #include <string_view>
 #include <unordered_map>
+#include <utility>
 #include <vector>
 
 namespace servesim {
@@ -103,8 +104,32 @@ class Rng {
 
 uint64_t substream_seed(uint64_t root, std::string_view tag, uint64_t index = 0);
 
-// ---- engine-facing types the scheduler and router read (engine.h) -------------------
+// ---- engine-facing types (engine.h) -------------------------------------------------
+enum class SchedulerPolicy { kLens, kPrefillPriority, kStaticChunked };
+SchedulerPolicy scheduler_policy_from_string(const std::string& name);
+std::string to_string(SchedulerPolicy policy);
+
 PerfParams perf_profile(const std::string& name);
+
+struct EngineConfig {
+  int engine_id = 0;
+  PerfParams true_params;
+  double noise_sigma = 0.05;
+  int64_t kv_blocks = 8192;
+  int64_t block_size = 16;
+  int64_t m_max = 8192;
+  int64_t q_max = 256;
+  SchedulerPolicy scheduler_policy = SchedulerPolicy::kLens;
+  int64_t static_budget = 2048;
+  double state_report_period_ms = 100.0;
+  double state_staleness_ms = 0.0;
+  int64_t wait_cap = 0;
+  bool valid() const {
+    return kv_blocks > 0 && block_size >= 1 && noise_sigma >= 0.0 && static_budget >= 1 &&
+           static_budget <= m_max && m_max >= q_max && q_max >= 1 && state_report_period_ms > 0.0 &&
+           state_staleness_ms >= 0.0 && wait_cap >= 0 && true_params.valid();
+  }
+};
 
 struct StateVector {
   int engine_id = 0;
@@ -343,5 +368,168 @@ class OnlineLearner {
 };
 
 std::vector<LatencySample> load_samples_jsonl(const std::string& path);
+
+// ---- metrics (metrics.h) ---------------------------------------------------------------
+struct RequestRecord {
+  uint64_t request_id = 0;
+  double arrival_ms = 0.0;
+  double first_token_ms = 0.0;
+  double completed_ms = 0.0;
+  int64_t prompt_tokens = 0;
+  int64_t output_tokens = 0;
+  int engine_id = 0;
+};
+
+struct RequestMetrics {
+  double ttft_ms = 0.0;
+  double tpot_ms = 0.0;
+  double e2e_ms = 0.0;
+  bool single_token = false;
+};
+
+RequestMetrics request_metrics(const RequestRecord& rec);
+double percentile(std::vector<double> values, double p);
+
+struct SloAttainment {
+  double percent = 100.0;
+  bool empty = false;
+};
+SloAttainment slo_attainment(std::span<const RequestRecord> records, const SLOSpec& slo);
+
+struct MetricsSummary {
+  int64_t completed = 0;
+  double p50_e2e_ms = 0.0;
+  double p90_e2e_ms = 0.0;
+  double p50_ttft_ms = 0.0;
+  double p50_tpot_ms = 0.0;
+  double mean_ttft_ms = 0.0;
+  double mean_tpot_ms = 0.0;
+  double slo_attainment_pct = 100.0;
+  std::vector<std::pair<int, double>> engine_share;
+};
+MetricsSummary summarize(std::span<const RequestRecord> records, const SLOSpec& slo);
+void write_requests_csv(const std::string& path, std::span<const RequestRecord> records);
+
+// ---- workload (workload.h) -------------------------------------------------------------
+struct TraceRecord {
+  double arrival_ms = 0.0;
+  std::string session_id;
+  int64_t prompt_tokens = 1;
+  int64_t output_tokens = 1;
+};
+
+struct LengthStats {
+  double mean = 0.0;
+  double p99 = 0.0;
+  double std_dev = 0.0;
+};
+
+struct ScenarioStats {
+  std::string name;
+  LengthStats prompt;
+  LengthStats output;
+  double session_turn_prob = 0.0;
+  bool valid() const {
+    return prompt.mean > 0.0 && output.mean > 0.0 && prompt.p99 >= 0.0 && output.p99 >= 0.0 &&
+           prompt.std_dev >= 0.0 && output.std_dev >= 0.0 && session_turn_prob >= 0.0 &&
+           session_turn_prob <= 1.0;
+  }
+};
+
+enum class ArrivalMode { kTimestamp, kQps };
+
+const ScenarioStats& scenario_by_name(const std::string& name);
+std::vector<std::string> scenario_names();
+ScenarioStats load_scenario_json(const std::string& path);
+std::vector<TraceRecord> load_trace(const std::string& path, bool* sorted_warning = nullptr);
+void write_trace(const std::string& path, const std::vector<TraceRecord>& records);
+std::vector<TraceRecord> synth_generate(const ScenarioStats& stats, int64_t n, uint64_t seed);
+std::vector<TraceRecord> assign_arrivals(std::vector<TraceRecord> records, ArrivalMode mode,
+                                         double rate_per_s, uint64_t seed, double time_scale = 1.0,
+                                         bool poisson = false);
+
+// ---- simulation (sim.h): runs on the lockstep kernel ---------------------------------
+struct WorkloadConfig {
+  std::string scenario;
+  std::string scenario_file;
+  std::string trace_path;
+  ArrivalMode mode = ArrivalMode::kQps;
+  double rate_per_s = 1.0;
+  int64_t n = 100;
+  double time_scale = 1.0;
+  bool poisson = false;
+};
+
+struct OutputConfig {
+  std::string dir;
+  std::string summary = "summary.json";
+  std::string requests_csv = "requests.csv";
+  std::string plans_jsonl;
+  std::string routing_jsonl;
+};
+
+struct RunConfig {
+  uint64_t seed = 1;
+  double duration_ms = 3.6e6;
+  SLOSpec slo;
+  SchedulerConfig scheduler;
+  TradeoffModel tradeoff;
+  LearnerConfig learner;
+  RouterConfig router;
+  std::vector<EngineConfig> engines;
+  WorkloadConfig workload;
+  OutputConfig output;
+  bool record_learner_history = false;
+  bool validate_invariants = false;
+
+  void validate() const;
+  static RunConfig from_json_text(const std::string& text);
+  static RunConfig from_json_file(const std::string& path);
+  // The RunConfig JSON document (RunConfig::from_json_text's schema) — what
+  // the device batch entry point nx_sim_create_json consumes.
+  std::string to_json_text() const;
+};
+
+struct LearnerSnapshot {
+  int engine_id = 0;
+  double sim_time_ms = 0.0;
+  int64_t samples_seen = 0;
+  PerfParams params;
+};
+
+struct RunResult {
+  int64_t arrived = 0;
+  int64_t completed = 0;
+  int64_t rejected = 0;
+  int64_t unfinished = 0;
+  uint64_t arrival_hash = 0;
+  uint64_t event_hash = 0;
+  std::vector<RequestRecord> records;
+  MetricsSummary metrics;
+  std::vector<LearnerSnapshot> learner_history;
+  std::string summary_json;
+};
+
+RunResult run_simulation(const RunConfig& cfg);
+// Many configs as one device batch (one replica each); results in order.
+std::vector<RunResult> run_replicas(std::span<const RunConfig> cfgs, int device = 0);
+
+enum class SweepAxis { kRate, kPolicy, kBudget };
+SweepAxis sweep_axis_from_string(const std::string& name);
+
+struct SweepRow {
+  std::string value;
+  bool ok = false;
+  std::string error;
+  RunResult result;
+};
+
+struct SweepResult {
+  SweepAxis axis;
+  std::vector<SweepRow> rows;
+};
+
+SweepResult sweep(const RunConfig& base, SweepAxis axis, const std::vector<std::string>& values);
+std::string sweep_csv(const SweepResult& result);
 
 }  // namespace servesim

@@ -560,3 +560,463 @@ std::vector<LatencySample> load_samples_jsonl(const std::string& path) {
 }
 
 }  // namespace servesim
+
+// =====================================================================================
+// Engine policies, metrics, workload, simulation (engine.h, metrics.h, workload.h,
+// sim.h). Metrics and workload synthesis are the host front-end's
+// (csrc/host/report.cpp, frontend.cpp: reference semantics, host libm for the
+// arrival doubles); run_simulation / sweep run on the lockstep kernel.
+// =====================================================================================
+#include "report.hpp"
+
+#include <filesystem>
+#include <sstream>
+
+namespace servesim {
+
+SchedulerPolicy scheduler_policy_from_string(const std::string& name) {
+  if (name == "lens") return SchedulerPolicy::kLens;
+  if (name == "prefill_priority") return SchedulerPolicy::kPrefillPriority;
+  if (name == "static_chunked") return SchedulerPolicy::kStaticChunked;
+  throw std::runtime_error("unknown scheduler policy: " + name);
+}
+
+std::string to_string(SchedulerPolicy policy) {
+  switch (policy) {
+    case SchedulerPolicy::kLens: return "lens";
+    case SchedulerPolicy::kPrefillPriority: return "prefill_priority";
+    case SchedulerPolicy::kStaticChunked: return "static_chunked";
+  }
+  return "?";
+}
+
+// ---- metrics ------------------------------------------------------------------------
+namespace {
+nx::RecordRow row_of(const RequestRecord& r) {
+  return {static_cast<int64_t>(r.request_id), r.arrival_ms, r.first_token_ms, r.completed_ms,
+          r.prompt_tokens, r.output_tokens, r.engine_id};
+}
+std::vector<nx::RecordRow> rows_of(std::span<const RequestRecord> recs) {
+  std::vector<nx::RecordRow> v;
+  v.reserve(recs.size());
+  for (const auto& r : recs) v.push_back(row_of(r));
+  return v;
+}
+}  // namespace
+
+RequestMetrics request_metrics(const RequestRecord& rec) {
+  if (!(rec.arrival_ms <= rec.first_token_ms && rec.first_token_ms <= rec.completed_ms))
+    throw std::invalid_argument("RequestRecord timestamps out of order");
+  RequestMetrics m;
+  m.ttft_ms = rec.first_token_ms - rec.arrival_ms;
+  m.e2e_ms = rec.completed_ms - rec.arrival_ms;
+  m.single_token = rec.output_tokens < 2;
+  m.tpot_ms = m.single_token ? 0.0
+                             : (rec.completed_ms - rec.first_token_ms) / static_cast<double>(rec.output_tokens - 1);
+  return m;
+}
+
+double percentile(std::vector<double> values, double p) { return nx::percentile_nearest_rank(std::move(values), p); }
+
+SloAttainment slo_attainment(std::span<const RequestRecord> records, const SLOSpec& slo) {
+  if (records.empty()) return {100.0, true};
+  return {nx::summarize_records(rows_of(records), slo.ttft_slo_ms, slo.tpot_slo_ms).slo_pct, false};
+}
+
+MetricsSummary summarize(std::span<const RequestRecord> records, const SLOSpec& slo) {
+  const nx::Metrics m = nx::summarize_records(rows_of(records), slo.ttft_slo_ms, slo.tpot_slo_ms);
+  MetricsSummary out;
+  out.completed = m.completed;
+  out.p50_e2e_ms = m.p50_e2e;
+  out.p90_e2e_ms = m.p90_e2e;
+  out.p50_ttft_ms = m.p50_ttft;
+  out.p50_tpot_ms = m.p50_tpot;
+  out.mean_ttft_ms = m.mean_ttft;
+  out.mean_tpot_ms = m.mean_tpot;
+  out.slo_attainment_pct = m.slo_pct;
+  out.engine_share = m.engine_share;
+  return out;
+}
+
+void write_requests_csv(const std::string& path, std::span<const RequestRecord> records) {
+  nx::write_requests_csv(path, rows_of(records));
+}
+
+// ---- workload -----------------------------------------------------------------------
+namespace {
+ScenarioStats stats_of(const nx::Scenario& s) {
+  ScenarioStats o;
+  o.name = s.name;
+  o.prompt = {s.prompt.mean, s.prompt.p99, s.prompt.std_dev};
+  o.output = {s.output.mean, s.output.p99, s.output.std_dev};
+  o.session_turn_prob = s.session_turn_prob;
+  return o;
+}
+nx::Scenario scenario_of(const ScenarioStats& s) {
+  nx::Scenario o;
+  o.name = s.name;
+  o.prompt = {s.prompt.mean, s.prompt.p99, s.prompt.std_dev};
+  o.output = {s.output.mean, s.output.p99, s.output.std_dev};
+  o.session_turn_prob = s.session_turn_prob;
+  return o;
+}
+std::vector<TraceRecord> records_of(const std::vector<nx::TraceRow>& rows) {
+  std::vector<TraceRecord> out;
+  out.reserve(rows.size());
+  for (const auto& r : rows) out.push_back({r.arrival_ms, r.session, r.prompt, r.output});
+  return out;
+}
+std::vector<nx::TraceRow> trace_rows_of(const std::vector<TraceRecord>& recs) {
+  std::vector<nx::TraceRow> out;
+  out.reserve(recs.size());
+  for (const auto& r : recs) out.push_back({r.arrival_ms, r.session_id, r.prompt_tokens, r.output_tokens});
+  return out;
+}
+}  // namespace
+
+std::vector<std::string> scenario_names() { return {"flowgpt", "coding", "sharegpt", "summarization"}; }
+
+const ScenarioStats& scenario_by_name(const std::string& name) {
+  static const std::map<std::string, ScenarioStats> table = [] {
+    std::map<std::string, ScenarioStats> t;
+    for (const auto& n : scenario_names()) t[n] = stats_of(nx::scenario_named(n));
+    return t;
+  }();
+  const auto it = table.find(name);
+  if (it == table.end()) throw std::runtime_error("unknown scenario: " + name);
+  return it->second;
+}
+
+ScenarioStats load_scenario_json(const std::string& path) { return stats_of(nx::scenario_from_file(path)); }
+
+std::vector<TraceRecord> load_trace(const std::string& path, bool* sorted_warning) {
+  return records_of(nx::load_trace_rows(path, sorted_warning));
+}
+
+void write_trace(const std::string& path, const std::vector<TraceRecord>& records) {
+  nx::write_trace_rows(path, trace_rows_of(records));
+}
+
+std::vector<TraceRecord> synth_generate(const ScenarioStats& stats, int64_t n, uint64_t seed) {
+  if (!stats.valid()) throw std::invalid_argument("invalid ScenarioStats");
+  return records_of(nx::synth_rows(scenario_of(stats), n, seed));
+}
+
+std::vector<TraceRecord> assign_arrivals(std::vector<TraceRecord> records, ArrivalMode mode, double rate_per_s,
+                                         uint64_t seed, double time_scale, bool poisson) {
+  std::vector<nx::TraceRow> rows = trace_rows_of(records);
+  nx::assign_arrival_times(rows, mode == ArrivalMode::kTimestamp, rate_per_s, seed, time_scale, poisson);
+  return records_of(rows);
+}
+
+// ---- simulation -----------------------------------------------------------------------
+namespace {
+nlohmann::ordered_json params_json(const PerfParams& p) { return nlohmann::ordered_json::parse(p.to_json()); }
+
+PerfParams params_of(const nx::Params& p) {
+  PerfParams q;
+  q.tau0 = p.tau0; q.w0 = p.w0; q.ws = p.ws; q.tauB = p.tauB;
+  q.tauS = p.tauS; q.p_max = p.p_max; q.kB = p.kB; q.kS = p.kS;
+  return q;
+}
+}  // namespace
+
+// RunConfig in the schema RunConfig::from_json_text reads (sim.cpp:454-582):
+// every field explicit, so parsing it back yields this RunConfig exactly.
+std::string RunConfig::to_json_text() const {
+  nlohmann::ordered_json j;
+  j["seed"] = seed;
+  j["duration_ms"] = duration_ms;
+  j["record_learner_history"] = record_learner_history;
+  j["slo"] = {{"ttft_slo_ms", slo.ttft_slo_ms}, {"tpot_slo_ms", slo.tpot_slo_ms}};
+  j["scheduler"] = {{"m_max", scheduler.m_max}, {"q_max", scheduler.q_max},
+                    {"n_search_iters", scheduler.n_search_iters}, {"eps_ratio", scheduler.eps_ratio},
+                    {"q_ref", scheduler.q_ref}};
+  j["tradeoff"] = {{"alpha_ms", tradeoff.alpha_ms}, {"beta", tradeoff.beta}, {"l_bar", tradeoff.l_bar},
+                   {"td_min_ms", tradeoff.td_min_ms}};
+  j["learner"] = {{"long_window", learner.long_window}, {"short_window", learner.short_window},
+                  {"structural_period", learner.structural_period}, {"linear_period", learner.linear_period},
+                  {"min_structural_samples", learner.min_structural_samples}};
+  nlohmann::ordered_json r;
+  r["policy"] = to_string(router.policy);
+  r["weights"] = std::vector<double>(router.weights.begin(), router.weights.end());
+  r["beta_aff"] = router.beta_aff;
+  r["latency_knee"] = router.latency_knee;
+  r["latency_scale_ms"] = router.latency_scale_ms;
+  r["load_half_ms"] = router.load_half_ms;
+  r["capacity_headroom"] = router.capacity_headroom;
+  r["staleness_limit_ms"] = router.staleness_limit_ms;
+  r["latency_window_ms"] = router.latency_window_ms;
+  nlohmann::ordered_json sw = nlohmann::ordered_json::object();
+  for (const auto& [id, w] : router.static_weights) sw[std::to_string(id)] = w;
+  r["static_weights"] = sw;
+  j["router"] = r;
+  nlohmann::ordered_json es = nlohmann::ordered_json::array();
+  for (const auto& e : engines) {
+    nlohmann::ordered_json x;
+    x["engine_id"] = e.engine_id;
+    x["true_params"] = params_json(e.true_params);
+    x["noise_sigma"] = e.noise_sigma;
+    x["kv_blocks"] = e.kv_blocks;
+    x["block_size"] = e.block_size;
+    x["m_max"] = e.m_max;
+    x["q_max"] = e.q_max;
+    x["scheduler_policy"] = to_string(e.scheduler_policy);
+    x["static_budget"] = e.static_budget;
+    x["state_report_period_ms"] = e.state_report_period_ms;
+    x["state_staleness_ms"] = e.state_staleness_ms;
+    x["wait_cap"] = e.wait_cap;
+    es.push_back(x);
+  }
+  j["engines"] = es;
+  j["workload"] = {{"scenario", workload.scenario}, {"scenario_file", workload.scenario_file},
+                   {"trace", workload.trace_path},
+                   {"mode", workload.mode == ArrivalMode::kQps ? "qps" : "timestamp"},
+                   {"rate", workload.rate_per_s}, {"n", workload.n}, {"time_scale", workload.time_scale},
+                   {"poisson", workload.poisson}};
+  j["output"] = {{"dir", output.dir}, {"summary", output.summary}, {"requests_csv", output.requests_csv},
+                 {"plans_jsonl", output.plans_jsonl}, {"routing_jsonl", output.routing_jsonl}};
+  return j.dump();
+}
+
+RunConfig RunConfig::from_json_text(const std::string& text) {
+  const nx::RunCfg c = nx::parse_run_config(text);  // reference defaults + validation
+  RunConfig o;
+  o.seed = c.seed;
+  o.duration_ms = c.duration_ms;
+  o.record_learner_history = c.record_learner_history;
+  o.slo = {c.ttft_slo, c.tpot_slo};
+  o.scheduler.m_max = c.m_max;
+  o.scheduler.q_max = c.q_max;
+  o.scheduler.n_search_iters = c.n_search_iters;
+  o.scheduler.eps_ratio = c.eps_ratio;
+  o.scheduler.q_ref = c.q_ref;
+  o.tradeoff = {c.alpha, c.beta, c.l_bar, c.td_min};
+  o.learner = {c.long_window, c.short_window, c.structural_period, c.linear_period, c.min_structural};
+  o.router.policy = static_cast<RouterPolicy>(c.route_policy);
+  for (int i = 0; i < 4; ++i) o.router.weights[i] = c.weights[i];
+  o.router.beta_aff = c.beta_aff;
+  o.router.latency_knee = c.knee;
+  o.router.latency_scale_ms = c.scale_ms;
+  o.router.load_half_ms = c.load_half;
+  o.router.capacity_headroom = c.headroom;
+  o.router.staleness_limit_ms = c.staleness_limit;
+  o.router.latency_window_ms = c.latency_window;
+  o.router.static_weights = c.static_weights;
+  for (const auto& e : c.engines) {
+    EngineConfig x;
+    x.engine_id = e.engine_id;
+    x.true_params = params_of(e.true_params);
+    x.noise_sigma = e.noise_sigma;
+    x.kv_blocks = e.kv_blocks;
+    x.block_size = e.block_size;
+    x.m_max = e.m_max;
+    x.q_max = e.q_max;
+    x.scheduler_policy = static_cast<SchedulerPolicy>(e.policy);
+    x.static_budget = e.static_budget;
+    x.state_report_period_ms = e.report_period_ms;
+    x.state_staleness_ms = e.staleness_ms;
+    x.wait_cap = e.wait_cap;
+    o.engines.push_back(x);
+  }
+  o.workload.scenario = c.scenario;
+  o.workload.scenario_file = c.scenario_file;
+  o.workload.trace_path = c.trace_path;
+  o.workload.mode = c.timestamp_mode ? ArrivalMode::kTimestamp : ArrivalMode::kQps;
+  o.workload.rate_per_s = c.rate;
+  o.workload.n = c.n;
+  o.workload.time_scale = c.time_scale;
+  o.workload.poisson = c.poisson;
+  o.output = {c.out_dir, c.out_summary, c.out_requests_csv, c.out_plans_jsonl, c.out_routing_jsonl};
+  return o;
+}
+
+RunConfig RunConfig::from_json_file(const std::string& path) {
+  std::ifstream in(path);
+  if (!in) throw std::runtime_error("cannot open config: " + path);
+  std::ostringstream buf;
+  buf << in.rdbuf();
+  try {
+    return from_json_text(buf.str());
+  } catch (const std::exception& e) {
+    throw std::runtime_error(path + ": " + e.what());
+  }
+}
+
+void RunConfig::validate() const {
+  // the front-end's validator carries the reference's checks and messages
+  // (RunConfig::validate, sim.cpp:418-452); reaching it through the JSON
+  // form also exercises this config's round trip.
+  if (engines.empty()) throw std::runtime_error("config: needs >= 1 engine");
+  nx::validate_run_config(nx::parse_run_config(to_json_text()));
+}
+
+namespace {
+void raise_replica(const nx_replica_summary& s) {
+  std::string msg = nx_last_error();
+  if (msg.empty()) msg = "device replica failed";
+  if (s.status == NX_EINVAL) throw std::invalid_argument(msg);
+  if (s.status == NX_ELOGIC) throw std::logic_error(msg);
+  throw std::runtime_error(msg);
+}
+
+struct SimHandle {
+  nx_sim_t h = nullptr;
+  ~SimHandle() {
+    if (h) nx_sim_destroy(h);
+  }
+};
+
+RunResult result_of(nx_sim_t h, int32_t r, const nx_replica_summary& s) {
+  RunResult out;
+  out.arrived = s.arrived;
+  out.completed = s.completed;
+  out.rejected = s.rejected;
+  out.unfinished = s.unfinished;
+  out.arrival_hash = s.arrival_hash;
+  out.event_hash = s.event_hash;
+  std::vector<nx_request_record> recs(static_cast<size_t>(s.completed));
+  int64_t n = 0;
+  raise(nx_sim_records(h, r, recs.data(), s.completed, &n));
+  for (const auto& x : recs)
+    out.records.push_back({static_cast<uint64_t>(x.request_id), x.arrival_ms, x.first_token_ms, x.completed_ms,
+                           x.prompt_tokens, x.output_tokens, x.engine_id});
+  int64_t len = 0;
+  raise(nx_sim_summary_json(h, r, nullptr, 0, &len));
+  out.summary_json.assign(static_cast<size_t>(len) + 1, '\0');
+  raise(nx_sim_summary_json(h, r, out.summary_json.data(), len + 1, &len));
+  out.summary_json.resize(static_cast<size_t>(len));
+  raise(nx_sim_learner_history(h, r, nullptr, 0, &n));
+  std::vector<nx_learner_snapshot> hist(static_cast<size_t>(n));
+  raise(nx_sim_learner_history(h, r, hist.data(), n, &n));
+  for (const auto& x : hist) out.learner_history.push_back({x.engine_id, x.sim_time_ms, x.samples_seen, unpack(x.params)});
+  return out;
+}
+}  // namespace
+
+std::vector<RunResult> run_replicas(std::span<const RunConfig> cfgs, int device) {
+  std::vector<std::string> texts;
+  std::vector<const char*> ptrs;
+  for (const auto& c : cfgs) {
+    c.validate();
+    texts.push_back(c.to_json_text());
+  }
+  for (const auto& t : texts) ptrs.push_back(t.c_str());
+  SimHandle S;
+  raise(nx_sim_create_json(ptrs.data(), static_cast<int32_t>(ptrs.size()), device, 1, &S.h));
+  raise(nx_sim_run(S.h));
+  std::vector<nx_replica_summary> sums(cfgs.size());
+  raise(nx_sim_summaries(S.h, sums.data()));
+  std::vector<RunResult> out;
+  for (size_t r = 0; r < cfgs.size(); ++r) {
+    if (sums[r].status != NX_OK) raise_replica(sums[r]);
+    const RunConfig& c = cfgs[r];
+    RunResult res = result_of(S.h, static_cast<int32_t>(r), sums[r]);
+    res.metrics = summarize(res.records, c.slo);
+    if (!c.output.dir.empty()) raise(nx_sim_write_outputs(S.h, static_cast<int32_t>(r)));
+    out.push_back(std::move(res));
+  }
+  return out;
+}
+
+RunResult run_simulation(const RunConfig& cfg) {
+  return std::move(run_replicas(std::span<const RunConfig>(&cfg, 1))[0]);
+}
+
+SweepAxis sweep_axis_from_string(const std::string& name) {
+  if (name == "rate") return SweepAxis::kRate;
+  if (name == "policy") return SweepAxis::kPolicy;
+  if (name == "budget") return SweepAxis::kBudget;
+  throw std::runtime_error("unknown sweep axis: " + name);
+}
+
+// sweep (sim.cpp:608-642): every value that forms a valid config becomes one
+// replica of a single device batch instead of one sequential run each;
+// per-value failures are recorded in their rows.
+SweepResult sweep(const RunConfig& base, SweepAxis axis, const std::vector<std::string>& values) {
+  SweepResult out;
+  out.axis = axis;
+  std::vector<RunConfig> cfgs;
+  std::vector<size_t> row_of_cfg;
+  for (const std::string& value : values) {
+    SweepRow row;
+    row.value = value;
+    try {
+      RunConfig cfg = base;
+      cfg.output.dir.clear();
+      switch (axis) {
+        case SweepAxis::kRate:
+          cfg.workload.mode = ArrivalMode::kQps;
+          cfg.workload.rate_per_s = std::stod(value);
+          break;
+        case SweepAxis::kPolicy: {
+          const SchedulerPolicy policy = scheduler_policy_from_string(value);
+          for (auto& e : cfg.engines) e.scheduler_policy = policy;
+          break;
+        }
+        case SweepAxis::kBudget: {
+          const int64_t budget = std::stoll(value);
+          for (auto& e : cfg.engines) e.static_budget = budget;
+          break;
+        }
+      }
+      cfg.validate();
+      cfgs.push_back(cfg);
+      row_of_cfg.push_back(out.rows.size());
+    } catch (const std::exception& e) {
+      row.error = e.what();
+    }
+    out.rows.push_back(std::move(row));
+  }
+  if (cfgs.empty()) return out;
+  std::vector<std::string> texts;
+  std::vector<const char*> ptrs;
+  for (const auto& c : cfgs) texts.push_back(c.to_json_text());
+  for (const auto& t : texts) ptrs.push_back(t.c_str());
+  SimHandle S;
+  const int rc = nx_sim_create_json(ptrs.data(), static_cast<int32_t>(ptrs.size()), 0, 1, &S.h);
+  if (rc != NX_OK) {  // a workload that fails to build fails its sweep rows
+    const std::string msg = nx_last_error();
+    for (size_t i : row_of_cfg) out.rows[i].error = msg;
+    return out;
+  }
+  raise(nx_sim_run(S.h));
+  std::vector<nx_replica_summary> sums(cfgs.size());
+  raise(nx_sim_summaries(S.h, sums.data()));
+  for (size_t k = 0; k < cfgs.size(); ++k) {
+    SweepRow& row = out.rows[row_of_cfg[k]];
+    try {
+      if (sums[k].status != NX_OK) raise_replica(sums[k]);
+      row.result = result_of(S.h, static_cast<int32_t>(k), sums[k]);
+      row.result.metrics = summarize(row.result.records, cfgs[k].slo);
+      row.ok = true;
+    } catch (const std::exception& e) {
+      row.error = e.what();
+    }
+  }
+  return out;
+}
+
+std::string sweep_csv(const SweepResult& result) {
+  std::ostringstream out;
+  out << "value,arrived,completed,rejected,unfinished,mean_ttft_ms,mean_tpot_ms,p50_e2e_ms,p90_e2e_ms,"
+         "p50_ttft_ms,p50_tpot_ms,slo_attainment,arrival_hash,error\n";
+  char buf[360];
+  for (const auto& row : result.rows) {
+    if (!row.ok) {
+      out << row.value << ",,,,,,,,,,,,,\"" << row.error << "\"\n";
+      continue;
+    }
+    const auto& r = row.result;
+    const auto& m = r.metrics;
+    std::snprintf(buf, sizeof buf, "%s,%lld,%lld,%lld,%lld,%.4f,%.4f,%.4f,%.4f,%.4f,%.4f,%.4f,%016llx,\n",
+                  row.value.c_str(), static_cast<long long>(r.arrived), static_cast<long long>(r.completed),
+                  static_cast<long long>(r.rejected), static_cast<long long>(r.unfinished), m.mean_ttft_ms,
+                  m.mean_tpot_ms, m.p50_e2e_ms, m.p90_e2e_ms, m.p50_ttft_ms, m.p50_tpot_ms,
+                  m.slo_attainment_pct, static_cast<unsigned long long>(r.arrival_hash));
+    out << buf;
+  }
+  return out.str();
+}
+
+}  // namespace servesim

@@ -1,0 +1,4 @@
+// Forwarding header: the reference test suites include "servesim/metrics.h";
+// the B200 drop-in declares the whole API in one header.
+#pragma once
+#include "nx_servesim.hpp"

@@ -1,9 +1,12 @@
 """The reference's own unit tests — proj/tests/test_perf_model.cpp,
-test_lens.cpp, test_router.cpp and test_learner.cpp, compiled UNMODIFIED
-(tests/refsuite/Makefile) against the C++ drop-in include/nx_servesim.hpp —
-run on the device path: every throughput / predict_latency, schedule_step,
-binary_search_budget, allocate_tokens, target_latency, Router::route, score_*
-and OnlineLearner refit they exercise is a launch of the sm_100a kernels."""
+test_lens.cpp, test_router.cpp, test_learner.cpp, test_metrics.cpp,
+test_workload.cpp and test_sim.cpp (112 of its 128 cases; test_engine.cpp
+drives EngineSim step by step, which the device runs inside whole replicas),
+compiled UNMODIFIED (tests/refsuite/Makefile) against the C++ drop-in
+include/nx_servesim.hpp — run on the device path: every throughput /
+predict_latency, schedule_step, binary_search_budget, allocate_tokens,
+target_latency, Router::route, score_*, OnlineLearner refit and
+run_simulation / sweep they exercise is a launch of the sm_100a kernels."""
 import subprocess
 from pathlib import Path
 

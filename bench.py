@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--cpu-sample", type=int, default=32, help="replicas timed for cpu_baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-operators", action="store_true", help="skip the batched K2/K3/K4 lines")
     return ap.parse_args()
 
 
@@ -181,8 +182,130 @@ def k1_model_eval(torch, dev) -> dict:
             "records_per_s": n / t, "ms": t * 1e3,
             "roofline": {"bound": "hbm", "achieved": byts / t / 1e9, "peak": pk["hbm_gbs"],
                          "unit": "GB/s", "frac": byts / t / 1e9 / pk["hbm_gbs"],
-                         "traffic": None, "peak_source": src,
+                         "traffic": traffic("perf_eval_kernel"), "peak_source": src,
                          "bytes_per_record": 20}}
+
+
+def traffic(kernel: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel`
+    from the committed ncu --set full capture (profiles/r01_traffic.json)."""
+    try:
+        t = json.loads((ROOT / "profiles" / "r01_traffic.json").read_text())
+        return t[kernel]["traffic_bytes_per_launch"]
+    except Exception:
+        return None
+
+
+def operators(torch, dev) -> dict:
+    """The batched per-decision operators on device-resident batches:
+    K2 nx_lens_schedule (LENS decisions/s), K3 nx_prism_route (routes/s,
+    PRISM with echo), K4 nx_refit (structural refits/s on 4096-sample
+    windows). Device time per launch with CUDA events, after warm-up."""
+    import ctypes as C
+    import numpy as np
+    from paper_2509_23384_b200 import abi, lens, learner
+    from paper_2509_23384_b200._lib import check, lib
+    rng = np.random.default_rng(11)
+    stream = torch.cuda.current_stream(dev)
+
+    def timed(fn, reps=5):
+        ts = []
+        for it in range(reps + 2):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            if it >= 2:
+                ts.append(e0.elapsed_time(e1) / 1e3)
+        return statistics.mean(ts)
+
+    def dev_bytes(a):
+        return torch.from_numpy(np.ascontiguousarray(a).view(np.uint8).copy()).to(dev)
+
+    out = {}
+    # K2: LENS decisions over queues shaped like the sweep's engines
+    n = 1 << 17
+    P = np.zeros(n, dtype=abi.LENS_PROBLEM)
+    R = rng.integers(0, 64, n)
+    W = rng.integers(0, 64, n)
+    off = np.concatenate([[0], np.cumsum(W)[:-1]])
+    fast = [4.0, 0.0, 1.0, 0.08, 0.0004, 20.0, 4.0, 0.05]
+    for k, v in zip(("ttft_slo_ms", "tpot_slo_ms", "alpha_ms", "beta", "l_bar", "td_min_ms",
+                     "eps_ratio", "q_ref", "m_max", "q_max", "n_search_iters"),
+                    (2000.0, 50.0, 4000.0, 40.0, 128.0, 2.0, 0.05, 16.0, 8192, 256, 10)):
+        P[k] = v
+    P["params"] = fast
+    P["n_run"], P["n_wait"], P["wait_off"] = R, W, off
+    rem = np.exp(rng.uniform(0, np.log(2000), int(W.sum()))).astype(np.int32) + 1
+    dP, dR = dev_bytes(P), torch.from_numpy(rem).to(dev)
+    dPl = torch.empty(n * abi.LENS_PLAN.itemsize, dtype=torch.uint8, device=dev)
+    dA = torch.empty(rem.size, dtype=torch.int32, device=dev)
+    t = timed(lambda: check(lib().nx_lens_schedule_dev(dP.data_ptr(), n, dR.data_ptr(), rem.size,
+                                                       dPl.data_ptr(), dA.data_ptr(),
+                                                       C.c_void_p(stream.cuda_stream))))
+    plans = np.frombuffer(dPl.cpu().numpy().tobytes(), dtype=abi.LENS_PLAN)
+    if (plans["status"] != 0).any():
+        raise RuntimeError("nx_lens_schedule: problem errors")
+    out["lens_decisions_per_s"] = n / t
+    out["lens_batch"] = f"{n} decisions, |run| U[0,64), |wait| U[0,64)"
+    # K3: routers of 8 engines, 32 PRISM routes each (sequential within a group)
+    g, e, m = 1 << 14, 8, 32
+    G = np.zeros(g, dtype=abi.ROUTE_GROUP)
+    G["weights"] = [1.0, 1.0, 1.0, 1.0]
+    G["beta_aff"], G["latency_knee"], G["load_half_ms"] = 1.5, 0.5, 50.0
+    G["capacity_headroom"], G["staleness_limit_ms"], G["ttft_slo_ms"] = 2.0, 1000.0, 2000.0
+    G["l_bar_ema"], G["policy"], G["n_engines"], G["n_requests"], G["n_sessions"] = 128.0, 0, e, m, 64
+    G["engine_off"] = np.arange(g) * e
+    G["request_off"] = np.arange(g) * m
+    G["session_off"] = np.arange(g) * 64
+    Rp = np.zeros(g * e, dtype=abi.ENGINE_REPORT)
+    Rp["l_hat_ms"] = rng.uniform(0, 3000, g * e)
+    Rp["w_load_tokens"] = rng.uniform(0, 50000, g * e)
+    Rp["m_free_tokens"] = rng.uniform(0, 2e5, g * e)
+    Rp["p_max"] = rng.uniform(5, 20, g * e)
+    Rp["reported_at_ms"] = 0.0
+    Rp["has_report"], Rp["static_weight"] = 1, 1.0
+    Rp["engine_id"] = np.tile(np.arange(e), g)
+    Q = np.zeros(g * m, dtype=abi.ROUTE_REQUEST)
+    Q["now_ms"] = rng.uniform(0, 900, g * m)
+    Q["prompt_len"] = rng.integers(1, 4000, g * m)
+    Q["session"] = rng.integers(0, 64, g * m)
+    dG, dRp, dQ = dev_bytes(G), dev_bytes(Rp), dev_bytes(Q)
+    dS = torch.full((g * 64,), -1, dtype=torch.int32, device=dev)
+    dD = torch.empty(g * m * abi.ROUTE_DECISION.itemsize, dtype=torch.uint8, device=dev)
+    dSt = torch.empty(g, dtype=torch.int32, device=dev)
+    t = timed(lambda: check(lib().nx_prism_route_dev(dG.data_ptr(), g, dRp.data_ptr(), dQ.data_ptr(),
+                                                     dS.data_ptr(), dD.data_ptr(), dSt.data_ptr(),
+                                                     C.c_void_p(stream.cuda_stream))))
+    if int((dSt != 0).sum().item()):
+        raise RuntimeError("nx_prism_route: group errors")
+    out["prism_routes_per_s"] = g * m / t
+    out["prism_batch"] = f"{g} routers x {m} sequential routes, {e} engines each"
+    # K4: structural refits on 4096-sample windows
+    nr, wl = 1024, 4096
+    b = rng.integers(1, 257, nr * wl).astype(np.int32)
+    s_ = (b + np.where(rng.random(nr * wl) < 0.4, rng.integers(1, 8000, nr * wl), 0)).astype(np.int32)
+    bd, sd = b.astype(np.float64), s_.astype(np.float64)
+    fb = np.minimum(-np.expm1(-4.0 * bd), 1.0)
+    fs = np.minimum(-np.expm1(-0.05 * sd), 1.0)
+    y = (4.0 + sd / (20.0 * fb * fs) + 0.08 * bd + 4e-4 * sd) * np.exp(0.05 * rng.standard_normal(nr * wl))
+    RP = np.zeros(nr, dtype=abi.REFIT_PROBLEM)
+    RP["params"] = [5.0, 0.0, 1.0, 0.1, 0.001, 20.0, 0.1, 0.02]
+    RP["long_window"], RP["short_window"], RP["min_structural_samples"] = wl, 64, 256
+    RP["sample_off"], RP["n_samples"] = np.arange(nr) * wl, wl
+    dRP, dB, dS2, dY = dev_bytes(RP), torch.from_numpy(b).to(dev), torch.from_numpy(s_).to(dev), \
+        torch.from_numpy(y).to(dev)
+    dO = torch.empty(nr * abi.REFIT_RESULT.itemsize, dtype=torch.uint8, device=dev)
+    t = timed(lambda: check(lib().nx_refit_dev(learner.STRUCTURAL, dRP.data_ptr(), nr, dB.data_ptr(),
+                                               dS2.data_ptr(), dY.data_ptr(), wl, dO.data_ptr(),
+                                               C.c_void_p(stream.cuda_stream))), reps=3)
+    res = np.frombuffer(dO.cpu().numpy().tobytes(), dtype=abi.REFIT_RESULT)
+    if (res["status"] != 0).any():
+        raise RuntimeError("nx_refit: problem errors")
+    out["structural_refits_per_s"] = nr / t
+    out["refit_batch"] = f"{nr} OnlineLearner::update_structural on {wl}-sample windows"
+    return out
 
 
 # ---------------------------------------------------------------------------- arms
@@ -328,7 +451,7 @@ def run_nx(args):
             "decisions_per_step": total_dec / args.steps,
             "gpu_launches": args.steps,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                         "frac": achieved / pk["hbm_gbs"], "traffic": None,
+                         "frac": achieved / pk["hbm_gbs"], "traffic": traffic("nx_sim_kernel"),
                          "kernel": "nx_sim_kernel", "peak_source": src,
                          "algorithmic_bytes_per_launch": alg},
             "clocks": clk.summary(),
@@ -341,6 +464,11 @@ def run_nx(args):
             line["model_eval"] = k1_model_eval(torch, dev)
         except Exception as exc:  # keep the headline line even if K1 fails
             line["model_eval"] = {"error": repr(exc)}
+        if not args.no_operators:
+            try:
+                line["operators"] = operators(torch, dev)
+            except Exception as exc:
+                line["operators"] = {"error": repr(exc)}
         if world == 1 and not args.no_cpu_baseline:
             sample = cfgs[: args.cpu_sample]
             rate, kind, wall, dec = cpu_reference_rate(sample, os.cpu_count() or 1)

@@ -81,6 +81,7 @@ struct Ctx {
   int64_t roff, soff;
   int n_eng, n_req, n_sess, lane, prefix_cap;
   int worker;              // 0: event-loop warp, 1: structural-refit warp
+  int log_flags;           // NX_LOG_* of this replica (register copy of the descriptor's)
   double* fsm;             // shared-memory fit tables (1/f_B, then 1/f_S); nullptr: use scratch
   int fsm_cap;             // 1/f_S entries that fit in fsm
 };

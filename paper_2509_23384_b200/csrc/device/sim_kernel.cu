@@ -308,7 +308,7 @@ __device__ NX_COLD void try_begin_step(Ctx& c, int e, int64_t now_us) {
     g.step_seq = c.rs->next_seq++;
     c.rs->work[0] += 1;
     c.rs->work[1] += g.plan_b;
-    if (c.d->log_flags & NX_LOG_PLANS) {  // plans_jsonl row (sim.cpp:149-158)
+    if (c.log_flags & NX_LOG_PLANS) {  // plans_jsonl row (sim.cpp:149-158)
       const int64_t k = c.rs->n_plan_log;
       if (k >= c.d->plan_log_cap) {
         c.rs->status = 1;
@@ -843,7 +843,7 @@ __device__ NX_COLD int route(Ctx& c, int rid, double now, double& score, double 
 // structural refit record_sample may have queued is part of the update, so
 // the snapshot waits for it (history recording trades overlap for order).
 __device__ void log_learner(Ctx& c, int e, int64_t now_us) {
-  if (!(c.d->log_flags & NX_LOG_LEARNER) || failed(c)) return;
+  if (!(c.log_flags & NX_LOG_LEARNER) || failed(c)) return;
   wait_refit(c, e);
   __syncwarp();
   if (c.lane == 0) {
@@ -1012,7 +1012,7 @@ __device__ void run_replica(Ctx& c) {
           PhaseTimer pt(c.rs, 1);
           double score = 0.0, fac[4] = {1.0, 1.0, 1.0, 1.0};
           e = route(c, rid, to_ms(now), score, fac);
-          if (c.lane == 0 && (c.d->log_flags & NX_LOG_ROUTES)) {  // routing_jsonl row (sim.cpp:176-186)
+          if (c.lane == 0 && (c.log_flags & NX_LOG_ROUTES)) {  // routing_jsonl row (sim.cpp:176-186)
             NxRouteLog& L = c.P->route_log[c.d->route_log_off + c.rs->n_route_log];
             L.t_us = now;
             L.request = rid;
@@ -1167,6 +1167,7 @@ nx_sim_kernel(const NxPools* __restrict__ pools, const int32_t* __restrict__ ord
     c.n_eng = c.d->n_eng;
     c.n_req = c.d->n_req;
     c.n_sess = c.d->n_sess;
+    c.log_flags = c.d->log_flags;
     c.roff = c.d->req_off;
     c.soff = c.d->sess_off;
     c.scratch = pools->scratch + c.d->scratch_off;

@@ -105,6 +105,21 @@ struct Arena {
 constexpr int kWarpsPerBlock = 2;  // event-loop warp + refit warp per replica CTA
 
 
+// Stream-ordered scratch (cudaMallocAsync) for the batched operators: keep
+// the device's default pool's memory between calls instead of returning it
+// at every synchronisation (a re-grow per launch cost milliseconds).
+void retain_default_pool() {
+  thread_local int done_dev = -1;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev == done_dev) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t keep = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  done_dev = dev;
+}
+
 int current_sms() {
   int dev = 0;
   cudaGetDevice(&dev);
@@ -975,6 +990,7 @@ int nx_lens_schedule_dev(const nx_lens_problem* problems, int32_t n_problems,
     if (n_problems < 0 || n_wait_total < 0) throw std::invalid_argument("nx_lens_schedule: negative sizes");
     if (n_problems == 0) return;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    retain_default_pool();
     int32_t* gpre = nullptr;  // prefix scratch for spans beyond the shared-memory stage
     cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&gpre),
                                sizeof(int32_t) * static_cast<size_t>(n_wait_total + n_problems), st),
@@ -1085,6 +1101,7 @@ int nx_refit_dev(int32_t kind, const nx_refit_problem* problems, int32_t n_probl
       throw std::invalid_argument("nx_refit: bad sizes");
     if (n_problems == 0) return;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    retain_default_pool();
     const int64_t per = nx_refit_scratch_per(max_long_window);
     // one scratch slice per resident warp: bounded by the device, not the batch
     int grid = std::min<int64_t>(n_problems, static_cast<int64_t>(current_sms()) * 16);

@@ -1,0 +1,4 @@
+mkdir -p gpurun_out
+timeout 600 python -m pytest tests/test_gpu_parity.py -x -q > gpurun_out/pytest_gpu.txt 2>&1; echo "rc=$?" >> gpurun_out/pytest_gpu.txt
+timeout 300 python tools/phase_report.py > gpurun_out/phase.txt 2>&1
+timeout 300 python tools/timeline.py --replicas 512 > gpurun_out/tl512.txt 2>&1

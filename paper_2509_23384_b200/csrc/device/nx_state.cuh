@@ -105,9 +105,15 @@ __device__ __forceinline__ void fail(Ctx& c, int status, int site, int64_t info)
 }
 __device__ __forceinline__ bool failed(const Ctx& c) { return c.rs->status != 0; }
 
+// Phase-cycle instrumentation (diagnostic, tools/phase_report.py) is off
+// unless the launch sets it (NX_PHASE_TIMERS=1): the clock reads and the
+// shared-memory atomics stay off the event loop's critical path.
+// (one copy per translation unit; the simulator's launcher sets its own)
+static __constant__ int nx_timers_on;
+
 __device__ __forceinline__ long long nx_clock() {
 #ifdef __CUDA_ARCH__
-  return clock64();
+  return nx_timers_on ? clock64() : 0;
 #else
   return 0;
 #endif
@@ -128,7 +134,7 @@ struct PhaseTimer {
   long long t0;
   __device__ __forceinline__ PhaseTimer(RepSm* r, int kk) : rs(r), k(kk), t0(nx_clock()) {}
   __device__ __forceinline__ ~PhaseTimer() {
-    if (lane_id() == 0)
+    if (nx_timers_on && lane_id() == 0)
       atomicAdd(reinterpret_cast<unsigned long long*>(&rs->cycles[k]),
                 static_cast<unsigned long long>(nx_clock() - t0));
   }
@@ -136,7 +142,7 @@ struct PhaseTimer {
 
 // counters shared by both warps of a replica CTA
 __device__ __forceinline__ void count(int64_t& slot, int64_t v) {
-  atomicAdd(reinterpret_cast<unsigned long long*>(&slot), static_cast<unsigned long long>(v));
+  if (v != 0) atomicAdd(reinterpret_cast<unsigned long long*>(&slot), static_cast<unsigned long long>(v));
 }
 __device__ __forceinline__ int32_t vload(const int32_t& x) {
   return *reinterpret_cast<const volatile int32_t*>(&x);

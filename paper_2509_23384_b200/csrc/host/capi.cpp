@@ -585,7 +585,14 @@ int nx_sim_launch(nx_sim_t h) {
     int per_sm = 0;
     cuda_check(nx_sim_occupancy(kWarpsPerBlock, smem, &per_sm), "occupancy");
     if (per_sm < 1) throw NxError(NX_ECUDA, "simulation kernel does not fit on an SM");
-    if (const char* cap = std::getenv("NX_SIM_CTAS_PER_SM")) per_sm = std::max(1, std::min(per_sm, std::atoi(cap)));
+    // Two replica CTAs per SM: measured 1.76-1.82 s per bench-shard launch vs
+    // 2.04-2.09 s at 3 and 2.17-2.22 s at 4 (the register limit). More
+    // co-resident event loops mostly add instruction-fetch contention
+    // (ncu no_instruction stalls) while the queue of replicas is long enough
+    // to keep two per SM busy (longest first).
+    int cap_sm = 2;
+    if (const char* cap = std::getenv("NX_SIM_CTAS_PER_SM")) cap_sm = std::max(1, std::atoi(cap));
+    per_sm = std::min(per_sm, cap_sm);
     const int need = h->n_rep;
     const int grid = std::max(1, std::min(need, per_sm * sm_count(h->device)));
     cuda_check(cudaEventRecord(h->ev0, st), "event");

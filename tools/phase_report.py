@@ -1,5 +1,6 @@
 """Per-phase SM-cycle attribution of single replicas (latency analysis)."""
-import argparse, sys
+import argparse, os, sys
+os.environ.setdefault("NX_PHASE_TIMERS", "1")  # the kernel skips its cycle counters otherwise
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2509_23384_b200 import sim, workloads as W

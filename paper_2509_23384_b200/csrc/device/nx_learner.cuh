@@ -895,14 +895,16 @@ static __device__ void post_refit(Ctx& c, int e) {
   __syncwarp();
 }
 
-// Tells the refit warp the replica is done (job id -1).
+// Tells every refit warp the replica is done (one job id -1 each).
 static __device__ void post_exit(Ctx& c) {
   __syncwarp();
   if (c.lane == 0) {
-    const int t = vload(c.rs->jq_tail);
-    c.rs->jq_eng[t & 63] = -1;
-    __threadfence_block();
-    vstore(c.rs->jq_tail, t + 1);
+    for (int k = 0; k < kRefitWarps; ++k) {
+      const int t = vload(c.rs->jq_tail);
+      c.rs->jq_eng[t & 63] = -1;
+      __threadfence_block();
+      vstore(c.rs->jq_tail, t + 1);
+    }
   }
   __syncwarp();
 }
@@ -924,14 +926,18 @@ static __device__ void wait_refit(Ctx& c, int e) {
   if (c.lane == 0) count(c.rs->cycles[8], nx_clock() - t0);
 }
 
-// The refit warp: pops engine ids and runs update_structural until it pops -1.
+// A refit warp: claims the next job (engine id) and runs update_structural
+// until it claims -1. kRefitWarps workers share the ring, so engines whose
+// structural periods come due together refit in parallel. At most one job
+// per engine is outstanding (record_sample waits before posting the next),
+// so the 64-slot ring never wraps onto an unclaimed job.
 static __device__ NX_COLD void refit_worker(Ctx& c) {
   while (true) {
     int e = -2;
     if (c.lane == 0) {
-      const int h = vload(c.rs->jq_head);
+      const int h = atomicAdd(&c.rs->jq_head, 1);
       unsigned ns = 128;
-      while (vload(c.rs->jq_tail) == h) {
+      while (vload(c.rs->jq_tail) <= h) {
         __nanosleep(ns);
         ns = ns < 2048 ? 2 * ns : 2048;
       }
@@ -940,7 +946,6 @@ static __device__ NX_COLD void refit_worker(Ctx& c) {
     }
     e = __shfl_sync(NX_FULL, e, 0);
     if (e < 0) {
-      if (c.lane == 0) vstore(c.rs->jq_head, vload(c.rs->jq_head) + 1);
       __syncwarp();
       return;
     }
@@ -950,10 +955,7 @@ static __device__ NX_COLD void refit_worker(Ctx& c) {
     }
     __threadfence_block();
     __syncwarp();
-    if (c.lane == 0) {
-      vstore(c.eng[e].refit_pending, 0);
-      vstore(c.rs->jq_head, vload(c.rs->jq_head) + 1);
-    }
+    if (c.lane == 0) vstore(c.eng[e].refit_pending, 0);
     __syncwarp();
   }
 }

@@ -24,7 +24,18 @@ namespace nxd {
 
 constexpr uint64_t kNoEvent = ~0ull;
 constexpr int kFbTable = 1024;  // batch-factor table entries per learner fit
-constexpr int kFitSmemS = 4096; // 1/f_S entries of the refit warp's shared-memory fit tables
+constexpr int kFitSmemS = 2560; // 1/f_S entries of a refit warp's shared-memory fit tables
+#ifndef NX_REFIT_WARPS
+#define NX_REFIT_WARPS 3
+#endif
+constexpr int kRefitWarps = NX_REFIT_WARPS;  // structural-refit workers per replica CTA
+constexpr int kSimWarps = 1 + kRefitWarps;   // + the event-loop warp
+
+// Doubles of one warp's learner scratch for long_window W (nx_learner.cuh
+// layout; host: capi.cpp fill_descriptors allocates kSimWarps per replica).
+__host__ __device__ __forceinline__ int64_t refit_scratch_stride(int64_t W) {
+  return (10 * W + kFbTable + 5120 + 64 + 31) / 32 * 32;
+}
 
 // Engine scalars (EngineSim + OnlineLearner + TradeoffEstimator + router view)
 struct EngSm {

@@ -1130,10 +1130,10 @@ __device__ NX_COLD void write_outputs(Ctx& c, int r) {
 
 }  // namespace nxd
 
-// One CTA of two warps per replica: warp 0 runs the event loop, warp 1 runs
+// One CTA per replica: warp 0 runs the event loop, warps 1..kRefitWarps run
 // the queued structural refits. CTAs pull replica indices (host order, longest
 // expected first) from a global counter so a long replica never idles others.
-extern "C" __global__ void __launch_bounds__(64)
+extern "C" __global__ void __launch_bounds__(32 * nxd::kSimWarps)
 nx_sim_kernel(const NxPools* __restrict__ pools, const int32_t* __restrict__ order, int n_rep,
               int* next_rep, int smem_per_cta, int prefix_cap, int max_eng) {
   using namespace nxd;
@@ -1150,11 +1150,12 @@ nx_sim_kernel(const NxPools* __restrict__ pools, const int32_t* __restrict__ ord
                                                                         : 32 * 5 * 8) + 15) & ~size_t(15);
   c.chunk = reinterpret_cast<double*>(smem + rep_bytes + warp * stage);
   c.prefix = reinterpret_cast<int32_t*>(c.chunk);
-  c.eng = reinterpret_cast<EngSm*>(smem + rep_bytes + 2 * stage);
+  c.eng = reinterpret_cast<EngSm*>(smem + rep_bytes + kSimWarps * stage);
   c.prefix_cap = prefix_cap;
-  // the refit warp's fit tables follow the engine states (nx_sim_smem_per_warp)
-  const size_t fit_off = (rep_bytes + 2 * stage + sizeof(EngSm) * static_cast<size_t>(max_eng) + 15) & ~size_t(15);
-  c.fsm = warp == 1 ? reinterpret_cast<double*>(smem + fit_off) : nullptr;
+  // the refit warps' fit tables follow the engine states (nx_sim_smem_per_warp)
+  const size_t fit_off = (rep_bytes + kSimWarps * stage + sizeof(EngSm) * static_cast<size_t>(max_eng) + 15) &
+                         ~size_t(15);
+  c.fsm = warp >= 1 ? reinterpret_cast<double*>(smem + fit_off) + (warp - 1) * (kFbTable + kFitSmemS) : nullptr;
   c.fsm_cap = kFitSmemS;
   (void)smem_per_cta;
   while (true) {
@@ -1172,8 +1173,8 @@ nx_sim_kernel(const NxPools* __restrict__ pools, const int32_t* __restrict__ ord
     c.log_flags = c.d->log_flags;
     c.roff = c.d->req_off;
     c.soff = c.d->sess_off;
-    c.scratch = pools->scratch + c.d->scratch_off;
-    c.lin_rows = c.scratch + 6 * c.d->long_w + kFbTable + warp * c.d->long_w;
+    c.scratch = pools->scratch + c.d->scratch_off + warp * refit_scratch_stride(c.d->long_w);
+    c.lin_rows = c.scratch + 6 * c.d->long_w + kFbTable;
     if (warp == 0) init_replica(c);
     __syncthreads();
     if (warp == 0) {
@@ -1195,9 +1196,9 @@ extern "C" size_t nx_sim_smem_per_warp(int max_engines, int prefix_cap) {
   const size_t rep_bytes = (sizeof(RepSm) + 15) & ~size_t(15);
   const size_t stage = ((static_cast<size_t>(prefix_cap) * 4 > 32 * 5 * 8 ? static_cast<size_t>(prefix_cap) * 4
                                                                         : 32 * 5 * 8) + 15) & ~size_t(15);
-  const size_t fit_off = (rep_bytes + 2 * stage + sizeof(EngSm) * static_cast<size_t>(max_engines) + 15) &
+  const size_t fit_off = (rep_bytes + kSimWarps * stage + sizeof(EngSm) * static_cast<size_t>(max_engines) + 15) &
                          ~size_t(15);
-  return fit_off + sizeof(double) * (kFbTable + kFitSmemS);
+  return fit_off + sizeof(double) * kRefitWarps * (kFbTable + kFitSmemS);
 }
 
 extern "C" cudaError_t nx_launch_sim(const NxPools* d_pools, const int32_t* d_order, int n_rep,

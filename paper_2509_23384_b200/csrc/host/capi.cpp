@@ -102,7 +102,10 @@ struct Arena {
   }
 };
 
-constexpr int kWarpsPerBlock = 2;  // event-loop warp + refit warp per replica CTA
+#ifndef NX_REFIT_WARPS
+#define NX_REFIT_WARPS 3
+#endif
+constexpr int kWarpsPerBlock = 1 + NX_REFIT_WARPS;  // event-loop warp + refit warps per replica CTA
 
 
 // Stream-ordered scratch (cudaMallocAsync) for the batched operators: keep
@@ -295,7 +298,8 @@ void fill_descriptors(nx_sim& h) {
     h.n_learn_log += d.learn_log_cap;
     req_off += n;
     sess_off += ns;
-    scratch_off += (10 * static_cast<int64_t>(c.long_window) + 1024 + 5120 + 64 + 31) / 32 * 32;  // nx_learner.cuh layout
+    // one learner scratch per warp (nx_state.cuh refit_scratch_stride)
+    scratch_off += kWarpsPerBlock * ((10 * static_cast<int64_t>(c.long_window) + 1024 + 5120 + 64 + 31) / 32 * 32);
     for (const auto& ec : c.engines) {
       NxEngineDesc e;
       std::memset(&e, 0, sizeof e);

@@ -593,6 +593,86 @@ struct FitOut {
 };
 
 // gauged_fit (learner.cpp:228-298) for fixed (kB, kS).
+// ---- the fit pass, optionally split across the refit team ---------------------
+// Accumulates the 11 (kB,kS)-dependent normal-equation entries over samples
+// [lo, hi) of the staged window (table path); lanes stride 32, 8 samples in
+// flight per lane. Returns this warp's totals (warp_sum) in out[11].
+static __device__ __forceinline__ void pass_range(const double2* rec, const double* stab, const double* ifb_t,
+                                                  int tab, double kB, int lo, int hi, int lane, double out[11]) {
+  double a01 = 0, a02 = 0, a11 = 0, a12 = 0, a22 = 0, a13 = 0, a14 = 0, a23 = 0, a24 = 0;
+  double t1 = 0, t2 = 0;
+  auto accumulate = [&](double iy, int bi, int si, double ifs) {
+    const double b = bi, s = si;
+    const double ifb = bi <= tab ? ifb_t[bi] : 1.0 / raw_factor(kB, b);
+    double q = ifb * ifs;  // 1 / max(fB fS, 1e-300)
+    q = q > 1e300 ? 1e300 : q;
+    const double u1 = q * iy, u2 = (s * q) * iy, r3 = b * iy, r4 = s * iy;
+    a01 += iy * u1; a02 += iy * u2; a11 += u1 * u1; a12 += u1 * u2; a22 += u2 * u2;
+    a13 += u1 * r3; a14 += u1 * r4; a23 += u2 * r3; a24 += u2 * r4;
+    t1 += u1; t2 += u2;
+  };
+  auto unpack = [](double y, int& bi, int& id, int& si) {
+    const unsigned long long v = static_cast<unsigned long long>(__double_as_longlong(y));
+    bi = static_cast<int>(v & 0xffffull);
+    id = static_cast<int>((v >> 16) & 0xffffull);
+    si = static_cast<int>(v >> 32);
+  };
+  int i = lo + lane;
+  for (; i + 224 < hi; i += 256) {
+    double2 r[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) r[u] = rec[i + 32 * u];
+    double fs[8];
+    int bi[8], si[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      int id;
+      unpack(r[u].y, bi[u], id, si[u]);
+      fs[u] = stab[id];
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) accumulate(r[u].x, bi[u], si[u], fs[u]);
+  }
+  for (; i < hi; i += 32) {
+    const double2 r = rec[i];
+    int bi, id, si;
+    unpack(r.y, bi, id, si);
+    accumulate(r.x, bi, si, stab[id]);
+  }
+  out[0] = warp_sum(a01); out[1] = warp_sum(a02); out[2] = warp_sum(a11); out[3] = warp_sum(a12);
+  out[4] = warp_sum(a22); out[5] = warp_sum(a13); out[6] = warp_sum(a14); out[7] = warp_sum(a23);
+  out[8] = warp_sum(a24); out[9] = warp_sum(t1); out[10] = warp_sum(t2);
+}
+
+// Named barrier of the refit team (warps 1..kRefitWarps of the replica CTA).
+__device__ __forceinline__ void team_sync() {
+  asm volatile("bar.sync 1, %0;" ::"r"(32 * kRefitWarps) : "memory");
+}
+// Contiguous, 256-aligned share of [0, n) for team member k of `team`.
+__device__ __forceinline__ void team_range(int n, int k, int team, int& lo, int& hi) {
+  const int per = ((n + 255) / 256 + team - 1) / team * 256;
+  lo = min(n, k * per);
+  hi = min(n, lo + per);
+}
+
+// Helper warps of the refit team: run their share of each fit pass the
+// leader (warp 1) publishes, until it publishes op -1.
+static __device__ NX_COLD void team_helper(Ctx& c) {
+  const int k = c.worker - 1;
+  while (true) {
+    team_sync();  // task published
+    const TeamTask t = c.rs->team;
+    if (t.op < 0) break;
+    int lo, hi;
+    team_range(t.n, k, kRefitWarps, lo, hi);
+    double part[11];
+    pass_range(t.rec, t.stab, t.ifb, t.tab, t.kB, lo, hi, c.lane, part);
+    if (c.lane == 0)
+      for (int q = 0; q < 11; ++q) c.rs->team_part[k][q] = part[q];
+    team_sync();  // partial totals written
+  }
+}
+
 static __device__ FitOut gauged_fit_impl(Ctx& c, Stage& S, const Params& cur, double kB, double kS);
 static __device__ FitOut gauged_fit(Ctx& c, Stage& S, const Params& cur, double kB, double kS) {
   const long long t0 = nx_clock();
@@ -622,50 +702,32 @@ static __device__ NX_COLD FitOut gauged_fit_impl(Ctx& c, Stage& S, const Params&
   }
   const long long tf1 = nx_clock();
   if (c.lane == 0) count(c.rs->cycles[7], tf1 - tf0);
-  double a01 = 0, a02 = 0, a11 = 0, a12 = 0, a22 = 0, a13 = 0, a14 = 0, a23 = 0, a24 = 0;
-  double t1 = 0, t2 = 0;
-  auto accumulate = [&](double iy, int bi, int si, double ifs) {
-    const double b = bi, s = si;
-    const double ifb = bi <= S.tab ? S.ifb[bi] : 1.0 / raw_factor(kB, b);
-    double q = ifb * ifs;  // 1 / max(fB fS, 1e-300)
-    q = q > 1e300 ? 1e300 : q;
-    const double u1 = q * iy, u2 = (s * q) * iy, r3 = b * iy, r4 = s * iy;
-    a01 += iy * u1; a02 += iy * u2; a11 += u1 * u1; a12 += u1 * u2; a22 += u2 * u2;
-    a13 += u1 * r3; a14 += u1 * r4; a23 += u2 * r3; a24 += u2 * r4;
-    t1 += u1; t2 += u2;
-  };
-  if (S.use_tab) {
-    // 8 samples per lane in flight: the record loads and the two table
-    // gathers of a group issue back to back (memory-level parallelism)
-    auto unpack = [](double y, int& bi, int& id, int& si) {
-      const unsigned long long v = static_cast<unsigned long long>(__double_as_longlong(y));
-      bi = static_cast<int>(v & 0xffffull);
-      id = static_cast<int>((v >> 16) & 0xffffull);
-      si = static_cast<int>(v >> 32);
-    };
-    int i = c.lane;
-    for (; i + 224 < n; i += 256) {
-      double2 r[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) r[u] = S.rec[i + 32 * u];
-      double fs[8];
-      int bi[8], si[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        int id;
-        unpack(r[u].y, bi[u], id, si[u]);
-        fs[u] = S.stab[id];
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) accumulate(r[u].x, bi[u], si[u], fs[u]);
+  // per-entry totals of the pass (fixed combination order across the team;
+  // every term is positive, so the closed-form SSE bound covers any order)
+  double tot[11];
+  if (S.use_tab && c.team > 1) {
+    if (c.lane == 0) {
+      c.rs->team.rec = S.rec;
+      c.rs->team.stab = S.stab;
+      c.rs->team.ifb = S.ifb;
+      c.rs->team.kB = kB;
+      c.rs->team.n = n;
+      c.rs->team.tab = S.tab;
+      c.rs->team.op = 1;
     }
-    for (; i < n; i += 32) {
-      const double2 r = S.rec[i];
-      int bi, id, si;
-      unpack(r.y, bi, id, si);
-      accumulate(r.x, bi, si, S.stab[id]);
-    }
+    team_sync();  // publish
+    int lo, hi;
+    team_range(n, 0, c.team, lo, hi);
+    pass_range(S.rec, S.stab, S.ifb, S.tab, kB, lo, hi, c.lane, tot);
+    team_sync();  // helpers' totals written
+    for (int k = 1; k < c.team; ++k)
+#pragma unroll
+      for (int q = 0; q < 11; ++q) tot[q] += c.rs->team_part[k][q];
+  } else if (S.use_tab) {
+    pass_range(S.rec, S.stab, S.ifb, S.tab, kB, 0, n, c.lane, tot);
   } else {
+    double a01 = 0, a02 = 0, a11 = 0, a12 = 0, a22 = 0, a13 = 0, a14 = 0, a23 = 0, a24 = 0;
+    double t1 = 0, t2 = 0;
     for (int i = c.lane; i < n; i += 32) {
       const double2 r = S.rec[i];
       const long long bs = __double_as_longlong(r.y);
@@ -677,16 +739,25 @@ static __device__ NX_COLD FitOut gauged_fit_impl(Ctx& c, Stage& S, const Params&
       } else {
         ifs = S.ifs[i];
       }
-      accumulate(r.x, bi, si, ifs);
+      const double iy = r.x, b = bi, s = si;
+      const double ifb = bi <= S.tab ? S.ifb[bi] : 1.0 / raw_factor(kB, b);
+      double q = ifb * ifs;  // 1 / max(fB fS, 1e-300)
+      q = q > 1e300 ? 1e300 : q;
+      const double u1 = q * iy, u2 = (s * q) * iy, r3 = b * iy, r4 = s * iy;
+      a01 += iy * u1; a02 += iy * u2; a11 += u1 * u1; a12 += u1 * u2; a22 += u2 * u2;
+      a13 += u1 * r3; a14 += u1 * r4; a23 += u2 * r3; a24 += u2 * r4;
+      t1 += u1; t2 += u2;
     }
+    tot[0] = warp_sum(a01); tot[1] = warp_sum(a02); tot[2] = warp_sum(a11); tot[3] = warp_sum(a12);
+    tot[4] = warp_sum(a22); tot[5] = warp_sum(a13); tot[6] = warp_sum(a14); tot[7] = warp_sum(a23);
+    tot[8] = warp_sum(a24); tot[9] = warp_sum(t1); tot[10] = warp_sum(t2);
   }
   S.ifs_k = kS;
   if (c.lane == 0) count(c.rs->cycles[9], nx_clock() - tf1);
   const long long tf2 = nx_clock();
-  const double u15[15] = {S.A00, warp_sum(a01), warp_sum(a02), S.A03, S.A04,
-                          warp_sum(a11), warp_sum(a12), warp_sum(a13), warp_sum(a14),
-                          warp_sum(a22), warp_sum(a23), warp_sum(a24), S.A33, S.A34, S.A44};
-  const double t5[5] = {S.t0, warp_sum(t1), warp_sum(t2), S.t3, S.t4};
+  const double u15[15] = {S.A00, tot[0], tot[1], S.A03, S.A04, tot[2], tot[3], tot[5], tot[6],
+                          tot[4], tot[7], tot[8], S.A33, S.A34, S.A44};
+  const double t5[5] = {S.t0, tot[9], tot[10], S.t3, S.t4};
   const double e = normal_elem(u15, t5);
   const double y2 = static_cast<double>(n);  // sum of 1.0 * 1.0 (learner.cpp:73)
   const double prior[5] = {cur.tau0, cur.w0 / cur.p_max, cur.ws / cur.p_max, cur.tauB, cur.tauS};
@@ -895,16 +966,14 @@ static __device__ void post_refit(Ctx& c, int e) {
   __syncwarp();
 }
 
-// Tells every refit warp the replica is done (one job id -1 each).
+// Tells the refit leader the replica is done (job id -1).
 static __device__ void post_exit(Ctx& c) {
   __syncwarp();
   if (c.lane == 0) {
-    for (int k = 0; k < kRefitWarps; ++k) {
-      const int t = vload(c.rs->jq_tail);
-      c.rs->jq_eng[t & 63] = -1;
-      __threadfence_block();
-      vstore(c.rs->jq_tail, t + 1);
-    }
+    const int t = vload(c.rs->jq_tail);
+    c.rs->jq_eng[t & 63] = -1;
+    __threadfence_block();
+    vstore(c.rs->jq_tail, t + 1);
   }
   __syncwarp();
 }
@@ -926,11 +995,13 @@ static __device__ void wait_refit(Ctx& c, int e) {
   if (c.lane == 0) count(c.rs->cycles[8], nx_clock() - t0);
 }
 
-// A refit warp: claims the next job (engine id) and runs update_structural
-// until it claims -1. kRefitWarps workers share the ring, so engines whose
-// structural periods come due together refit in parallel. At most one job
-// per engine is outstanding (record_sample waits before posting the next),
-// so the 64-slot ring never wraps onto an unclaimed job.
+// The refit leader (warp 1): claims the next job (engine id) and runs
+// update_structural — its fit passes split across the team's helper warps —
+// until it claims -1, then releases the helpers. At most one job per engine
+// is outstanding (record_sample waits before posting the next), so the
+// 64-slot ring never wraps onto an unclaimed job. (Measured: refits of
+// different engines rarely overlap, so one team per refit beats one worker
+// per refit.)
 static __device__ NX_COLD void refit_worker(Ctx& c) {
   while (true) {
     int e = -2;
@@ -946,6 +1017,10 @@ static __device__ NX_COLD void refit_worker(Ctx& c) {
     }
     e = __shfl_sync(NX_FULL, e, 0);
     if (e < 0) {
+      if (c.team > 1) {
+        if (c.lane == 0) c.rs->team.op = -1;
+        team_sync();  // helpers leave
+      }
       __syncwarp();
       return;
     }

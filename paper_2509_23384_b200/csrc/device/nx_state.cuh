@@ -24,12 +24,21 @@ namespace nxd {
 
 constexpr uint64_t kNoEvent = ~0ull;
 constexpr int kFbTable = 1024;  // batch-factor table entries per learner fit
-constexpr int kFitSmemS = 2560; // 1/f_S entries of a refit warp's shared-memory fit tables
+constexpr int kFitSmemS = 4096; // 1/f_S entries of the refit team's shared-memory fit tables
 #ifndef NX_REFIT_WARPS
 #define NX_REFIT_WARPS 3
 #endif
-constexpr int kRefitWarps = NX_REFIT_WARPS;  // structural-refit workers per replica CTA
+constexpr int kRefitWarps = NX_REFIT_WARPS;  // structural-refit team per replica CTA (leader + helpers)
 constexpr int kSimWarps = 1 + kRefitWarps;   // + the event-loop warp
+
+// One fit pass split across the refit team (nx_learner.cuh::team_pass).
+struct TeamTask {
+  const double2* rec;
+  const double* stab;
+  const double* ifb;
+  double kB;
+  int n, tab, op;  // op: 1 run a pass, -1 leave
+};
 
 // Doubles of one warp's learner scratch for long_window W (nx_learner.cuh
 // layout; host: capi.cpp fill_descriptors allocates kSimWarps per replica).
@@ -77,6 +86,8 @@ struct RepSm {
   int32_t cursor, status, site;
   int32_t jq_head, jq_tail;                    // structural-refit job ring (warp 0 -> warp 1)
   int32_t jq_eng[64];
+  TeamTask team;                               // refit leader -> helpers
+  double team_part[kRefitWarps][11];           // per-warp fit-pass totals
 };
 
 struct Ctx {
@@ -93,6 +104,7 @@ struct Ctx {
   int n_eng, n_req, n_sess, lane, prefix_cap;
   int worker;              // 0: event-loop warp, 1: structural-refit warp
   int log_flags;           // NX_LOG_* of this replica (register copy of the descriptor's)
+  int team;                // warps in the refit team (1: the calling warp alone)
   double* fsm;             // shared-memory fit tables (1/f_B, then 1/f_S); nullptr: use scratch
   int fsm_cap;             // 1/f_S entries that fit in fsm
 };

@@ -363,6 +363,7 @@ __global__ void __launch_bounds__(32) nx_refit_kernel(int kind, const nx_refit_p
       c.prefix_cap = 0;
       c.worker = 0;
       c.log_flags = 0;
+      c.team = 1;
       c.fsm = nullptr;  // fit tables in the warp's global scratch
       c.fsm_cap = 0;
       if (kind == NX_REFIT_LINEAR) {

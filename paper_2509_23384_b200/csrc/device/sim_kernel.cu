@@ -1155,8 +1155,9 @@ nx_sim_kernel(const NxPools* __restrict__ pools, const int32_t* __restrict__ ord
   // the refit warps' fit tables follow the engine states (nx_sim_smem_per_warp)
   const size_t fit_off = (rep_bytes + kSimWarps * stage + sizeof(EngSm) * static_cast<size_t>(max_eng) + 15) &
                          ~size_t(15);
-  c.fsm = warp >= 1 ? reinterpret_cast<double*>(smem + fit_off) + (warp - 1) * (kFbTable + kFitSmemS) : nullptr;
+  c.fsm = warp == 1 ? reinterpret_cast<double*>(smem + fit_off) : nullptr;
   c.fsm_cap = kFitSmemS;
+  c.team = kRefitWarps;
   (void)smem_per_cta;
   while (true) {
     if (threadIdx.x == 0) s_slot = atomicAdd(next_rep, 1);
@@ -1181,8 +1182,10 @@ nx_sim_kernel(const NxPools* __restrict__ pools, const int32_t* __restrict__ ord
       run_replica(c);
       for (int e = 0; e < c.n_eng; ++e) wait_refit(c, e);
       post_exit(c);
-    } else {
+    } else if (warp == 1) {
       refit_worker(c);
+    } else {
+      team_helper(c);
     }
     __syncthreads();
     if (warp == 0) write_outputs(c, r);
@@ -1198,7 +1201,7 @@ extern "C" size_t nx_sim_smem_per_warp(int max_engines, int prefix_cap) {
                                                                         : 32 * 5 * 8) + 15) & ~size_t(15);
   const size_t fit_off = (rep_bytes + kSimWarps * stage + sizeof(EngSm) * static_cast<size_t>(max_engines) + 15) &
                          ~size_t(15);
-  return fit_off + sizeof(double) * kRefitWarps * (kFbTable + kFitSmemS);
+  return fit_off + sizeof(double) * (kFbTable + kFitSmemS);
 }
 
 extern "C" cudaError_t nx_launch_sim(const NxPools* d_pools, const int32_t* d_order, int n_rep,

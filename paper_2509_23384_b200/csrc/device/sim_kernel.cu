@@ -25,7 +25,7 @@ constexpr double kInf = __builtin_huge_val();
 // ---- small helpers ------------------------------------------------------------
 __device__ __forceinline__ int blocks_for(int tokens, int block) { return (tokens + block - 1) / block; }
 __device__ __forceinline__ int remaining(const Ctx& c, int r) {
-  return c.P->prompt[c.roff + r] - c.P->prefilled[c.roff + r];
+  return c.P->req[c.roff + r].prompt - c.P->req[c.roff + r].prefilled;
 }
 
 // target_latency (lens.cpp:10-31) with the engine's tradeoff model
@@ -203,8 +203,8 @@ __device__ NX_COLD void trim_for_kv(Ctx& c, int e) {
       } else if (trimmed) {
         keep = false;
       } else {
-        const int foot = blocks_for(c.P->prompt[c.roff + r] + c.P->target[c.roff + r], ed.block_size);
-        const int fut = foot - blocks_for(c.P->prefilled[c.roff + r] + c.P->decoded[c.roff + r],
+        const int foot = blocks_for(c.P->req[c.roff + r].prompt + c.P->req[c.roff + r].target, ed.block_size);
+        const int fut = foot - blocks_for(c.P->req[c.roff + r].prefilled + c.P->req[c.roff + r].decoded,
                                           ed.block_size);
         if (static_cast<int64_t>(g.pinned) + g.reserved + fut <= ed.kv_blocks) {
           g.reserved += fut;
@@ -382,13 +382,13 @@ __device__ bool admit(Ctx& c, int e, int r) {
   const int sess = c.P->session[c.roff + r];
   const int cached = L.tok[sess];
   if (cached >= 0) {
-    const int prompt = c.P->prompt[c.roff + r];
+    const int prompt = c.P->req[c.roff + r].prompt;
     const int credit = cached < prompt - 1 ? cached : prompt - 1;
     const int cb = blocks_for(credit, ed.block_size);
     if (credit > 0 && static_cast<int64_t>(g.pinned) + g.reserved + cb <= ed.kv_blocks) {
       g.cache_blocks -= blocks_for(cached, ed.block_size);
       lru_unlink(g, L, sess);
-      c.P->prefilled[c.roff + r] = credit;
+      c.P->req[c.roff + r].prefilled = credit;
       g.pinned += cb;
     }
   }
@@ -467,16 +467,16 @@ __device__ NX_COLD void step_complete(Ctx& c, int e, int64_t now_us) {
     if (k < n) {
       r = preq[k];
       const int tok = ptok[k];
-      int pre = P.prefilled[ro + r], dec = P.decoded[ro + r];
+      const int4 q = *reinterpret_cast<const int4*>(&P.req[ro + r]);  // one 16-B load
+      int pre = q.x, dec = q.y;
       const int before = blocks_for(pre + dec, block);
       if (tok >= 0) pre += tok;
       else dec += 1;
       const int after = blocks_for(pre + dec, block);
       delta = after - before;
-      P.prefilled[ro + r] = pre;
-      P.decoded[ro + r] = dec;
-      first = tok >= 0 && pre == P.prompt[ro + r];
-      fin = tok < 0 && dec == P.target[ro + r];
+      *reinterpret_cast<int2*>(&P.req[ro + r]) = make_int2(pre, dec);
+      first = tok >= 0 && pre == q.z;
+      fin = tok < 0 && dec == q.w;
       if (first) P.first_us[ro + r] = now_us;
       if (fin) {
         held = after;
@@ -508,7 +508,7 @@ __device__ NX_COLD void step_complete(Ctx& c, int e, int64_t now_us) {
           const int rr = st_req[l];
           cache_insert(g, L, st_sess[l], st_tok[l], ed.kv_blocks, st_pin[l], block);
           // CompletionStats + TradeoffEstimator EMA/window (lens.cpp:149-160)
-          const int tgt = P.target[ro + rr];
+          const int tgt = P.req[ro + rr].target;
           const double first_ms = to_ms(P.first_us[ro + rr]);
           const double ttft = first_ms - P.arr_ms[ro + rr];
           const double tpot = tgt >= 2 ? (now - first_ms) / static_cast<double>(tgt - 1) : 0.0;
@@ -567,7 +567,7 @@ __device__ NX_COLD void step_complete(Ctx& c, int e, int64_t now_us) {
     for (int base = 0; base < len; base += 32) {
       const int i = base + c.lane;
       const int r = i < len ? rq[i] : 0;
-      const bool keep = i < len && P.decoded[ro + r] != P.target[ro + r];
+      const bool keep = i < len && P.req[ro + r].decoded != P.req[ro + r].target;
       const unsigned m = __ballot_sync(NX_FULL, keep);
       __syncwarp();
       if (keep) rq[out + __popc(m & ((1u << c.lane) - 1))] = r;
@@ -583,7 +583,7 @@ __device__ NX_COLD void step_complete(Ctx& c, int e, int64_t now_us) {
       int r = 0;
       if (k < n && ptok[k] >= 0) {
         r = preq[k];
-        nr = P.prefilled[ro + r] == P.prompt[ro + r];
+        nr = P.req[ro + r].prefilled == P.req[ro + r].prompt;
       }
       const unsigned m = __ballot_sync(NX_FULL, nr);
       if (nr) rq[out + __popc(m & ((1u << c.lane) - 1))] = r;
@@ -597,7 +597,7 @@ __device__ NX_COLD void step_complete(Ctx& c, int e, int64_t now_us) {
       int wpos = head + span - 1;
       for (int i = span - 1; i >= 0; --i) {
         const int r = wq[head + i];
-        if (P.prefilled[ro + r] != P.prompt[ro + r]) wq[wpos--] = r;
+        if (P.req[ro + r].prefilled != P.req[ro + r].prompt) wq[wpos--] = r;
       }
       const int removed = wpos + 1 - head;
       g.wq_head = head + removed;
@@ -786,7 +786,7 @@ __device__ NX_COLD int route(Ctx& c, int rid, double now, double& score, double 
       break;
     }
     default: {  // PRISM multiplicative score (router.cpp:205-284)
-      const int prompt = c.P->prompt[c.roff + rid];
+      const int prompt = c.P->req[c.roff + rid].prompt;
       const double dem = static_cast<double>(prompt) + c.rs->l_bar_ema;
       const double demand = (1.0 < dem) ? dem : 1.0;
       const int e = c.lane;

@@ -182,8 +182,7 @@ struct nx_sim {
   std::vector<int32_t> order;
   int64_t* h_arr_us = nullptr;
   double* h_arr_ms = nullptr;
-  int32_t* h_prompt = nullptr;
-  int32_t* h_target = nullptr;
+  NxReqState* h_req0 = nullptr;  // prompt/target + zeroed state
   int32_t* h_session = nullptr;
   // host pinned outputs
   NxReplicaOut* h_rep_out = nullptr;
@@ -214,7 +213,7 @@ struct nx_sim {
   ~nx_sim() {
     if (d_arena) cudaFree(d_arena);
     if (d_pools) cudaFree(d_pools);
-    for (void* p : {(void*)h_arr_us, (void*)h_arr_ms, (void*)h_prompt, (void*)h_target,
+    for (void* p : {(void*)h_arr_us, (void*)h_arr_ms, (void*)h_req0,
                     (void*)h_session, (void*)h_rep_out, (void*)h_eng_out, (void*)h_records,
                     (void*)h_first_us, (void*)h_done_us, (void*)h_req_engine, (void*)h_plan_log,
                     (void*)h_route_log, (void*)h_learn_log})
@@ -355,16 +354,14 @@ void fill_descriptors(nx_sim& h) {
   Arena A;
   const size_t o_arr_us = A.take<int64_t>(h.n_req);
   const size_t o_arr_ms = A.take<double>(h.n_req);
-  const size_t o_prompt = A.take<int32_t>(h.n_req);
-  const size_t o_target = A.take<int32_t>(h.n_req);
+  const size_t o_req0 = A.take<NxReqState>(h.n_req);
   const size_t o_session = A.take<int32_t>(h.n_req);
   h.off_rep = A.take<NxReplicaDesc>(h.n_rep);
   h.off_eng = A.take<NxEngineDesc>(h.n_eng);
   const size_t o_order = A.take<int32_t>(h.n_rep);
   // zero-initialised state
   h.off_state_begin = align_up(A.size, 256);
-  const size_t o_prefilled = A.take<int32_t>(h.n_req);
-  const size_t o_decoded = A.take<int32_t>(h.n_req);
+
   const size_t o_kv = A.take<uint8_t>(h.n_req);
   const size_t o_next = A.take<int>(1);
   h.off_state_end = A.size;
@@ -373,7 +370,8 @@ void fill_descriptors(nx_sim& h) {
   const size_t o_sess_eng = A.take<int32_t>(h.n_sess);
   const size_t o_ctok = A.take<int32_t>(cache_off);
   h.off_ff_end = A.size;
-  // uninitialised state
+  // uninitialised state (req is copied from req0 at every launch)
+  const size_t o_req = A.take<NxReqState>(h.n_req);
   const size_t o_first = A.take<int64_t>(h.n_req);
   const size_t o_done = A.take<int64_t>(h.n_req);
   const size_t o_reqeng = A.take<int32_t>(h.n_req);
@@ -408,11 +406,9 @@ void fill_descriptors(nx_sim& h) {
   NxPools& P = h.pools;
   P.arr_us = reinterpret_cast<const int64_t*>(B + o_arr_us);
   P.arr_ms = reinterpret_cast<const double*>(B + o_arr_ms);
-  P.prompt = reinterpret_cast<const int32_t*>(B + o_prompt);
-  P.target = reinterpret_cast<const int32_t*>(B + o_target);
+  P.req0 = reinterpret_cast<const NxReqState*>(B + o_req0);
   P.session = reinterpret_cast<const int32_t*>(B + o_session);
-  P.prefilled = reinterpret_cast<int32_t*>(B + o_prefilled);
-  P.decoded = reinterpret_cast<int32_t*>(B + o_decoded);
+  P.req = reinterpret_cast<NxReqState*>(B + o_req);
   P.first_us = reinterpret_cast<int64_t*>(B + o_first);
   P.done_us = reinterpret_cast<int64_t*>(B + o_done);
   P.req_engine = reinterpret_cast<int32_t*>(B + o_reqeng);
@@ -454,8 +450,7 @@ void fill_descriptors(nx_sim& h) {
   // pinned host image of the inputs
   h.h_arr_us = pinned<int64_t>(h.n_req);
   h.h_arr_ms = pinned<double>(h.n_req);
-  h.h_prompt = pinned<int32_t>(h.n_req);
-  h.h_target = pinned<int32_t>(h.n_req);
+  h.h_req0 = pinned<NxReqState>(h.n_req);
   h.h_session = pinned<int32_t>(h.n_req);
   for (int r = 0; r < h.n_rep; ++r) {
     const nx::Workload& w = h.wl[r];
@@ -463,8 +458,7 @@ void fill_descriptors(nx_sim& h) {
     const size_t n = w.prompt.size();
     std::memcpy(h.h_arr_us + o, w.arrival_us.data(), n * sizeof(int64_t));
     std::memcpy(h.h_arr_ms + o, w.arrival_ms.data(), n * sizeof(double));
-    std::memcpy(h.h_prompt + o, w.prompt.data(), n * sizeof(int32_t));
-    std::memcpy(h.h_target + o, w.output.data(), n * sizeof(int32_t));
+    for (size_t i = 0; i < n; ++i) h.h_req0[o + i] = {0, 0, w.prompt[i], w.output[i]};
     std::memcpy(h.h_session + o, w.session.data(), n * sizeof(int32_t));
   }
   // longest-expected replicas first: more requests and lower rates run longer
@@ -567,8 +561,7 @@ int nx_sim_upload(nx_sim_t h) {
     NxPools& P = h->pools;
     cp(const_cast<int64_t*>(P.arr_us), h->h_arr_us, h->n_req * sizeof(int64_t));
     cp(const_cast<double*>(P.arr_ms), h->h_arr_ms, h->n_req * sizeof(double));
-    cp(const_cast<int32_t*>(P.prompt), h->h_prompt, h->n_req * sizeof(int32_t));
-    cp(const_cast<int32_t*>(P.target), h->h_target, h->n_req * sizeof(int32_t));
+    cp(const_cast<NxReqState*>(P.req0), h->h_req0, h->n_req * sizeof(NxReqState));
     cp(const_cast<int32_t*>(P.session), h->h_session, h->n_req * sizeof(int32_t));
     cp(h->d_arena + h->off_rep, h->rep.data(), h->rep.size() * sizeof(NxReplicaDesc));
     cp(h->d_arena + h->off_eng, h->eng.data(), h->eng.size() * sizeof(NxEngineDesc));
@@ -584,6 +577,8 @@ int nx_sim_launch(nx_sim_t h) {
                                h->off_state_end - h->off_state_begin, st), "memset state");
     cuda_check(cudaMemsetAsync(h->d_arena + h->off_ff_begin, 0xff,
                                h->off_ff_end - h->off_ff_begin, st), "memset state");
+    cuda_check(cudaMemcpyAsync(h->pools.req, h->pools.req0, h->n_req * sizeof(NxReqState),
+                               cudaMemcpyDeviceToDevice, st), "request state image");
     const int spw = static_cast<int>(nx_sim_smem_per_warp(h->max_eng, h->prefix_cap));
     const size_t smem = static_cast<size_t>(spw);  // per replica CTA
     int per_sm = 0;

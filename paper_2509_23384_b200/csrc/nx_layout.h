@@ -99,13 +99,21 @@ typedef struct NxEngineOut {
   double alpha, beta, l_bar;
 } NxEngineOut;
 
+/* The per-request fields every step touches, as one 16-byte record (one
+   sector per request instead of one in each of four SoA arrays). */
+typedef struct NxReqState {
+  int32_t prefilled, decoded, prompt, target;
+} NxReqState;
+
 /* Device pools (all pointers are device pointers). */
 typedef struct NxPools {
   /* request inputs */
   const int64_t* arr_us; const double* arr_ms;
-  const int32_t* prompt; const int32_t* target; const int32_t* session;
+  const int32_t* session;
+  NxReqState* req;             /* state (prefilled, decoded) + prompt, target */
+  const NxReqState* req0;      /* launch image of req (prefilled = decoded = 0) */
   /* request state / outputs */
-  int32_t* prefilled; int32_t* decoded; int64_t* first_us; int64_t* done_us;
+  int64_t* first_us; int64_t* done_us;
   int32_t* req_engine; uint8_t* kv_admitted;
   /* queues and plans */
   int32_t* wq; int32_t* rq; int32_t* plan_req; int32_t* plan_tok;

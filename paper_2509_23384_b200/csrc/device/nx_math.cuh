@@ -46,6 +46,40 @@ static __device__ __noinline__ double expm1_neg(double kx) { return -expm1(-kx);
 #else
 __device__ __forceinline__ double expm1_neg(double kx) { return -expm1(-kx); }
 #endif
+// 1 - e^-x for x in [0, kSatArg): a branch-free expm1 for the streaming
+// evaluator (K1), ~22 instructions instead of libm's general expm1. With
+// y = -x = k ln2 + r, |r| <= ln2/2: expm1(y) = 2^k expm1(r) + (2^k - 1), and
+// expm1(r) = r + r^2 P(r) with the degree-13 Taylor polynomial (truncation
+// below 1e-17 relative). Within ~1 ulp of the correctly rounded value; K1's
+// contract is 1e-9 relative in fp64 mode, and the simulator keeps libm's
+// expm1 (bit-for-bit decisions are certified against it).
+__device__ __forceinline__ double one_minus_exp_neg(double x) {
+  const double y = -x;
+  const double kd = rint(y * 1.4426950408889634);           // y / ln2
+  const double r0 = fma(-kd, 6.93147180369123816490e-01, y); // ln2 hi
+  const double r = fma(-kd, 1.90821492927058770002e-10, r0); // ln2 lo
+  double p = 1.0 / 6227020800.0;                             // 1/13!
+  p = fma(p, r, 1.0 / 479001600.0);
+  p = fma(p, r, 1.0 / 39916800.0);
+  p = fma(p, r, 1.0 / 3628800.0);
+  p = fma(p, r, 1.0 / 362880.0);
+  p = fma(p, r, 1.0 / 40320.0);
+  p = fma(p, r, 1.0 / 5040.0);
+  p = fma(p, r, 1.0 / 720.0);
+  p = fma(p, r, 1.0 / 120.0);
+  p = fma(p, r, 1.0 / 24.0);
+  p = fma(p, r, 1.0 / 6.0);
+  p = fma(p, r, 0.5);
+  const double em = fma(r * r, p, r);                        // expm1(r)
+  const double s = __longlong_as_double(static_cast<long long>(1023 + static_cast<int>(kd)) << 52);  // 2^k
+  return fma(-s, em, 1.0 - s);                               // -(2^k em + 2^k - 1)
+}
+__device__ __forceinline__ double sat_fast(double k, double x) {
+  const double kx = k * x;
+  const double f = one_minus_exp_neg(kx);
+  return kx >= kSatArg ? kFactorMax : (f < kFactorMax ? f : kFactorMax);
+}
+
 __device__ __forceinline__ double raw_factor(double k, double x) {
   const double kx = k * x;
   return kx >= kSatArg ? 1.0 : expm1_neg(kx);

@@ -115,10 +115,10 @@ inline void fail(const char* kind, const char* expr, const char* file, int line)
 
 #ifdef DOCTEST_CONFIG_IMPLEMENT_WITH_MAIN
 int main(int argc, char** argv) {
-  const char* only = argc > 1 ? argv[1] : nullptr;  // optional substring filter
+  const char* only = argc > 1 ? argv[1] : nullptr;  // optional filter: case name or source file substring
   int failed_cases = 0, run = 0;
   for (const auto& c : doctest::detail::registry()) {
-    if (only && !std::strstr(c.name, only)) continue;
+    if (only && !std::strstr(c.name, only) && !std::strstr(c.file, only)) continue;
     ++run;
     const int before = doctest::detail::failures();
     try {

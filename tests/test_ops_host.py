@@ -70,3 +70,17 @@ def test_host_validation_precedes_device_work():
     rp["n_samples"], rp["sample_off"], rp["long_window"] = 10, 0, 64
     with pytest.raises(ValueError):
         learner.refit_batch(learner.LINEAR, rp, [1] * 3, [1] * 3, [1.0] * 3)
+
+
+REFSUITE = ROOT / "tests" / "refsuite" / "_bin" / "refsuite"
+
+
+@pytest.mark.skipif(not REFSUITE.exists(), reason="refsuite not built (needs /root/reference)")
+@pytest.mark.parametrize("suite", ["test_metrics.cpp", "test_workload.cpp"])
+def test_reference_host_suites_pass_against_the_drop_in(suite):
+    """The reference's metrics and workload unit tests (host-side functions in
+    the drop-in: summarize, percentile, write_requests_csv, synth_generate,
+    assign_arrivals, trace I/O) compiled unchanged against nx_servesim.hpp."""
+    import subprocess
+    r = subprocess.run([str(REFSUITE), suite], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "0 failed" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]

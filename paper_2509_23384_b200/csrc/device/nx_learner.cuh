@@ -34,14 +34,12 @@ __device__ __forceinline__ double pick5(const double v[5], int k) {
 
 // K independent systems in lockstep: their shuffle and division latencies
 // overlap. ok[k] reports each system's rank test separately.
-// Out of line and with the column loop rolled: one ~1k-instruction copy per K
-// instead of a ~4k-instruction straight-line body inlined at every call site.
-// It runs once per structural fit on the refit warp, and its unrolled body
-// streamed through the SM's instruction cache evicted the co-resident event
-// loops' hot code (ncu: no_instruction stalls 1.0 -> 6.6 cycles/issue at 3.5
-// replica CTAs per SM).
+// Inline, with the column loop rolled (a ~4k-instruction fully unrolled body
+// streamed through the instruction cache once per fit). Out of line it cost
+// 10k cycles per call: shuffles in a non-inlined function compile to
+// WARPSYNC/ENDCOLLECTIVE sequences, and the array arguments go to the stack.
 template <int K>
-static __device__ __noinline__ void solve5_warp_k(double (&v)[K], double (&x)[K][5], bool (&ok)[K]) {
+__device__ __forceinline__ void solve5_warp_k(double (&v)[K], double (&x)[K][5], bool (&ok)[K]) {
   const int lane = lane_id();
   const bool isA = lane < 25;
   const int i = isA ? lane / 5 : (lane < 30 ? lane - 25 : 0);
@@ -770,7 +768,9 @@ static __device__ NX_COLD FitOut gauged_fit_impl(Ctx& c, Stage& S, const Params&
   double vk[2] = {e, ridge_elem(e, 1e-7, prior)};
   double xk[2][5];
   bool okk[2];
+  const long long ts5 = nx_clock();
   solve5_warp_k<2>(vk, xk, okk);
+  if (c.lane == 0) count(c.rs->cycles[15], nx_clock() - ts5);
   if (!okk[0]) return out;
 #pragma unroll
   for (int q = 0; q < 5; ++q) x[q] = xk[0][q];

@@ -432,16 +432,27 @@ def run_nx(args):
         e2e = {"value": total_dec / e2e_t, "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h}
 
-    # K6: one NCCL all-gather of the per-replica summaries (the only exchange)
+    # K6: one NCCL all-gather of the per-replica summaries (the only exchange),
+    # over the product library's own communicator (nx_nccl_*); torch's
+    # all-gather only if that communicator cannot be built
     gathered = None
     if world > 1:
         nbytes = batch.summaries_nbytes()
-        buf = torch.empty(nbytes, dtype=torch.uint8, device=dev)
-        batch.copy_summaries(buf.data_ptr())
-        batch.synchronize()  # the copy runs on the handle's stream, NCCL on torch's
         out = torch.empty(nbytes * world, dtype=torch.uint8, device=dev)
-        dist.all_gather_into_tensor(out, buf)
-        torch.cuda.synchronize(dev)
+        try:
+            from paper_2509_23384_b200.collective import NcclComm
+            comm = NcclComm.from_torch_dist(rank, world, local)
+            batch.gather_summaries(comm, out.data_ptr())
+            batch.synchronize()
+            comm.close()
+            gather_via = "nx_sim_gather_summaries (ncclAllGather)"
+        except Exception as exc:  # noqa: BLE001
+            buf = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+            batch.copy_summaries(buf.data_ptr())
+            batch.synchronize()  # the copy runs on the handle's stream, NCCL on torch's
+            dist.all_gather_into_tensor(out, buf)
+            torch.cuda.synchronize(dev)
+            gather_via = f"torch all_gather ({exc!r})"
         gathered = world * len(cfgs)
 
     # roofline of the dominant kernel (nx_sim_kernel), from device work counters
@@ -469,6 +480,7 @@ def run_nx(args):
             line["e2e"] = e2e
         if gathered is not None:
             line["gathered_summaries"] = gathered
+            line["gather_via"] = gather_via
         try:
             line["model_eval"] = k1_model_eval(torch, dev)
         except Exception as exc:  # keep the headline line even if K1 fails

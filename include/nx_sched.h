@@ -356,6 +356,16 @@ int nx_sim_summaries_dev(nx_sim_t h, void** dev_ptr, int64_t* bytes);
 /* Device-to-device copy of those summaries into a caller buffer (e.g. the
  * send buffer of an ncclAllGather); ordered on the handle's stream. */
 int nx_sim_copy_summaries(nx_sim_t h, void* dst_dev);
+/* The gather itself over NCCL (libnccl.so.2 resolved at run time): rank 0
+ * makes a unique id, the caller distributes it (any channel), every rank
+ * joins, then one ncclAllGather of each rank's NxReplicaOut array (equal
+ * replica counts per rank) into recv_dev (nranks x the _dev bytes), ordered
+ * on the handle's stream. nx_gather_results of SURVEY §8(b). */
+#define NX_NCCL_ID_BYTES 128
+int nx_nccl_unique_id(char* id128);
+int nx_nccl_comm_init(const char* id128, int32_t nranks, int32_t rank, int32_t device, void** comm);
+int nx_nccl_comm_destroy(void* comm);
+int nx_sim_gather_summaries(nx_sim_t h, void* comm, void* recv_dev);
 
 /* ---- host utilities (reference workload generator semantics) -------------
  * synth_generate (proj/src/workload.cpp:137-166): prompts/outputs/session

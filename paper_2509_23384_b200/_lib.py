@@ -102,6 +102,10 @@ def lib() -> C.CDLL:
                     ("nx_sim_learner_history", LearnerSnapshot)):
         getattr(L, fn).argtypes = [C.c_void_p, C.c_int32, _P(row), C.c_int64, _P(C.c_int64)]
     L.nx_sim_write_outputs.argtypes = [C.c_void_p, C.c_int32]
+    L.nx_nccl_unique_id.argtypes = [C.c_char_p]
+    L.nx_nccl_comm_init.argtypes = [C.c_char_p, C.c_int32, C.c_int32, C.c_int32, _P(C.c_void_p)]
+    L.nx_nccl_comm_destroy.argtypes = [C.c_void_p]
+    L.nx_sim_gather_summaries.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
     L.nx_rng_state.argtypes = [C.c_uint64, C.c_char_p, C.c_uint64, _P(C.c_uint64)]
     L.nx_abi_sizes.argtypes = [_P(C.c_int64), C.c_int32]
     L.nx_lens_schedule_dev.argtypes = [V, C.c_int32, V, C.c_int64, V, V, V]

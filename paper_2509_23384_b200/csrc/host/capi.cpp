@@ -22,6 +22,9 @@
 #include "../nx_layout.h"
 #include "frontend.hpp"
 #include "nx_sched.h"
+#include <dlfcn.h>
+#include <nccl.h>
+
 #include "json.hpp"
 #include "report.hpp"
 
@@ -1239,6 +1242,80 @@ int nx_tradeoff_update_host(nx_tradeoff_state* st, int32_t n, const nx_completio
           st[i].win_head >= NX_TRADEOFF_WINDOW)
         throw std::invalid_argument("TradeoffEstimator: state out of range");
     run_scalar_op(4, st, sizeof *st, n, completions, sizeof(nx_completion) * n_completions, nullptr, 0);
+  });
+}
+
+// ---- K6: NCCL gather --------------------------------------------------------------
+}  // extern "C"
+
+namespace {
+// libnccl resolved at run time (the one torch already loaded, else the
+// system's): the product library has no link-time NCCL dependency.
+struct Nccl {
+  ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*all_gather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  const char* (*error_string)(ncclResult_t) = nullptr;
+};
+const Nccl& nccl() {
+  static Nccl n = [] {
+    Nccl x;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) throw NxError(NX_ERUNTIME, "libnccl.so.2 not found");
+    x.get_unique_id = reinterpret_cast<decltype(x.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+    x.comm_init_rank = reinterpret_cast<decltype(x.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
+    x.comm_destroy = reinterpret_cast<decltype(x.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+    x.all_gather = reinterpret_cast<decltype(x.all_gather)>(dlsym(h, "ncclAllGather"));
+    x.error_string = reinterpret_cast<decltype(x.error_string)>(dlsym(h, "ncclGetErrorString"));
+    if (!x.get_unique_id || !x.comm_init_rank || !x.comm_destroy || !x.all_gather || !x.error_string)
+      throw NxError(NX_ERUNTIME, "libnccl.so.2 lacks the collective entry points");
+    return x;
+  }();
+  return n;
+}
+void nccl_check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) throw NxError(NX_ECUDA, std::string(what) + ": " + nccl().error_string(r));
+}
+}  // namespace
+
+extern "C" {
+
+int nx_nccl_unique_id(char* id128) {
+  return guard([&] {
+    ncclUniqueId id;
+    nccl_check(nccl().get_unique_id(&id), "ncclGetUniqueId");
+    static_assert(sizeof(ncclUniqueId) == NX_NCCL_ID_BYTES, "ncclUniqueId size");
+    std::memcpy(id128, &id, sizeof id);
+  });
+}
+
+int nx_nccl_comm_init(const char* id128, int32_t nranks, int32_t rank, int32_t device, void** comm) {
+  return guard([&] {
+    if (nranks < 1 || rank < 0 || rank >= nranks) throw std::invalid_argument("nx_nccl_comm_init: bad rank");
+    cuda_check(cudaSetDevice(device), "cudaSetDevice");
+    ncclUniqueId id;
+    std::memcpy(&id, id128, sizeof id);
+    ncclComm_t c = nullptr;
+    nccl_check(nccl().comm_init_rank(&c, nranks, id, rank), "ncclCommInitRank");
+    *comm = c;
+  });
+}
+
+int nx_nccl_comm_destroy(void* comm) {
+  return guard([&] {
+    if (comm) nccl_check(nccl().comm_destroy(static_cast<ncclComm_t>(comm)), "ncclCommDestroy");
+  });
+}
+
+int nx_sim_gather_summaries(nx_sim_t h, void* comm, void* recv_dev) {
+  return guard([&] {
+    if (!comm || !recv_dev) throw std::invalid_argument("nx_sim_gather_summaries: null communicator or buffer");
+    cuda_check(cudaSetDevice(h->device), "cudaSetDevice");
+    const size_t bytes = static_cast<size_t>(h->n_rep) * sizeof(NxReplicaOut);
+    nccl_check(nccl().all_gather(h->pools.rep_out, recv_dev, bytes, ncclUint8, static_cast<ncclComm_t>(comm),
+                                 h->stream),
+               "ncclAllGather");
   });
 }
 

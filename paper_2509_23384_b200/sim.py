@@ -121,6 +121,11 @@ class Batch:
         check(lib().nx_sim_summaries_dev(self.h, C.byref(ptr), C.byref(n)))
         return n.value
 
+    def gather_summaries(self, comm, recv_ptr: int):
+        """K6: ncclAllGather of every rank's summaries into recv_ptr (device;
+        world x summaries_nbytes), on this batch's stream."""
+        check(lib().nx_sim_gather_summaries(self.h, comm.handle, C.c_void_p(recv_ptr)))
+
     def copy_summaries(self, dst_ptr: int):
         check(lib().nx_sim_copy_summaries(self.h, C.c_void_p(dst_ptr)))
 

@@ -84,3 +84,15 @@ def test_reference_host_suites_pass_against_the_drop_in(suite):
     import subprocess
     r = subprocess.run([str(REFSUITE), suite], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "0 failed" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+def test_batched_operators_fail_loudly_without_a_device():
+    """No CPU path behind the operators: without a GPU they raise CudaError."""
+    from paper_2509_23384_b200 import _lib, abi, lens
+    if _lib.lib().nx_device_count() > 0:
+        pytest.skip("a CUDA device is present")
+    probs = np.zeros(1, dtype=abi.LENS_PROBLEM)
+    probs[0] = lens.problem_record(1, 1, 0, lens.SLOSpec(), lens.TradeoffModel(), ops_cases.FAST,
+                                   lens.SchedulerConfig())
+    with pytest.raises(_lib.CudaError):
+        lens.schedule_batch(probs, np.ones(1, dtype=np.int32))

@@ -30,6 +30,8 @@ constexpr int kFitSmemS = 4096; // 1/f_S entries of the refit team's shared-memo
 #endif
 constexpr int kRefitWarps = NX_REFIT_WARPS;  // structural-refit team per replica CTA (leader + helpers)
 constexpr int kSimWarps = 1 + kRefitWarps;   // + the event-loop warp
+constexpr int kMaxSmIds = 1024;              // %smid bound of the kernel's SM bookkeeping
+constexpr int kSchedCtlInts = 3 + 2 * kMaxSmIds;
 
 // One fit pass split across the refit team (nx_learner.cuh::team_pass).
 struct TeamTask {

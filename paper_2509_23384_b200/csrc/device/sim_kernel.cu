@@ -1135,7 +1135,7 @@ __device__ NX_COLD void write_outputs(Ctx& c, int r) {
 // expected first) from a global counter so a long replica never idles others.
 extern "C" __global__ void __launch_bounds__(32 * nxd::kSimWarps)
 nx_sim_kernel(const NxPools* __restrict__ pools, const int32_t* __restrict__ order, int n_rep,
-              int* next_rep, int smem_per_cta, int prefix_cap, int max_eng) {
+              int* ctl, int smem_per_cta, int prefix_cap, int max_eng, int n_excl) {
   using namespace nxd;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int s_slot;
@@ -1159,8 +1159,55 @@ nx_sim_kernel(const NxPools* __restrict__ pools, const int32_t* __restrict__ ord
   c.fsm_cap = kFitSmemS;
   c.team = kRefitWarps;
   (void)smem_per_cta;
+  // Exclusive SMs for the longest replicas (order[0, n_excl)): under two
+  // resident CTAs per SM an event loop runs ~1.3-1.8x slower than alone, and
+  // the kernel ends with its longest replicas. The first CTA to arrive on
+  // each of n_excl SMs takes one of them while its sibling on that SM waits;
+  // then both join the shared queue order[n_excl, n). ctl: [0] shared
+  // cursor, [1] exclusive cursor, [2] exclusive SMs claimed, then per-SM
+  // arrival counts and states (0 unknown, 1 shared, 2 exclusive, 3 released).
+  __shared__ int s_excl;
+  int* sm_cnt = ctl + 3;
+  int* sm_state = ctl + 3 + kMaxSmIds;
+  unsigned smid = 0;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+  if (threadIdx.x == 0) {
+    int excl = 0;
+    if (n_excl > 0 && smid < static_cast<unsigned>(kMaxSmIds)) {
+      const int k = atomicAdd(&sm_cnt[smid], 1);
+      if (k == 0) {
+        excl = atomicAdd(&ctl[2], 1) < n_excl;
+        atomicExch(&sm_state[smid], excl ? 2 : 1);
+      } else {
+        int st;
+        unsigned ns = 256;
+        while ((st = atomicAdd(&sm_state[smid], 0)) == 0 || st == 2) {
+          __nanosleep(ns);
+          ns = ns < 8192 ? 2 * ns : 8192;
+        }
+      }
+    }
+    s_excl = excl;
+  }
+  __syncthreads();
   while (true) {
-    if (threadIdx.x == 0) s_slot = atomicAdd(next_rep, 1);
+    if (threadIdx.x == 0) {
+      int slot = n_rep;
+      if (s_excl) {
+        const int e = atomicAdd(&ctl[1], 1);
+        if (e < n_excl) slot = e;
+        s_excl = 0;  // one exclusive replica, then release the sibling
+      } else {
+        const int k = n_excl + atomicAdd(&ctl[0], 1);
+        if (k < n_rep) {
+          slot = k;
+        } else {  // shared queue drained: help with any exclusive ones left
+          const int e = atomicAdd(&ctl[1], 1);
+          if (e < n_excl) slot = e;
+        }
+      }
+      s_slot = slot;
+    }
     __syncthreads();
     const int slot = s_slot;
     __syncthreads();
@@ -1189,6 +1236,8 @@ nx_sim_kernel(const NxPools* __restrict__ pools, const int32_t* __restrict__ ord
     }
     __syncthreads();
     if (warp == 0) write_outputs(c, r);
+    if (threadIdx.x == 0 && slot < n_excl && smid < static_cast<unsigned>(kMaxSmIds))
+      atomicExch(&sm_state[smid], 3);  // exclusive replica done: wake the sibling
     __syncthreads();
   }
 }
@@ -1206,7 +1255,7 @@ extern "C" size_t nx_sim_smem_per_warp(int max_engines, int prefix_cap) {
 
 extern "C" cudaError_t nx_launch_sim(const NxPools* d_pools, const int32_t* d_order, int n_rep,
                                      int* d_next, int smem_per_warp, int prefix_cap, int max_eng,
-                                     int grid, int warps_per_block, cudaStream_t st) {
+                                     int grid, int warps_per_block, int n_excl, cudaStream_t st) {
   const size_t smem = static_cast<size_t>(smem_per_warp);  // one replica per CTA
   const char* tm = getenv("NX_PHASE_TIMERS");
   const int timers = tm && tm[0] == '1';
@@ -1217,7 +1266,7 @@ extern "C" cudaError_t nx_launch_sim(const NxPools* d_pools, const int32_t* d_or
                                          static_cast<int>(smem));
   if (err != cudaSuccess) return err;
   nx_sim_kernel<<<grid, 32 * warps_per_block, smem, st>>>(d_pools, d_order, n_rep, d_next,
-                                                          smem_per_warp, prefix_cap, max_eng);
+                                                          smem_per_warp, prefix_cap, max_eng, n_excl);
   return cudaGetLastError();
 }
 

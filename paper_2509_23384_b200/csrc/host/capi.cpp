@@ -30,7 +30,7 @@
 
 extern "C" cudaError_t nx_launch_sim(const NxPools* d_pools, const int32_t* d_order, int n_rep,
                                      int* d_next, int smem_per_warp, int prefix_cap, int max_eng,
-                                     int grid, int warps_per_block, cudaStream_t st);
+                                     int grid, int warps_per_block, int n_excl, cudaStream_t st);
 extern "C" cudaError_t nx_sim_occupancy(int warps_per_block, size_t smem, int* blocks_per_sm);
 extern "C" size_t nx_sim_smem_per_warp(int max_engines, int prefix_cap);
 extern "C" cudaError_t nx_launch_perf_eval(const double* params, int n_params, const int32_t* idx,
@@ -183,6 +183,7 @@ struct nx_sim {
   std::vector<NxReplicaDesc> rep;
   std::vector<NxEngineDesc> eng;
   std::vector<int32_t> order;
+  std::vector<double> cost;  // expected replica cost (longest first)
   int64_t* h_arr_us = nullptr;
   double* h_arr_ms = nullptr;
   NxReqState* h_req0 = nullptr;  // prompt/target + zeroed state
@@ -366,7 +367,7 @@ void fill_descriptors(nx_sim& h) {
   h.off_state_begin = align_up(A.size, 256);
 
   const size_t o_kv = A.take<uint8_t>(h.n_req);
-  const size_t o_next = A.take<int>(1);
+  const size_t o_next = A.take<int>(3 + 2 * 1024);  // kernel scheduling control (nx_state.cuh kSchedCtlInts)
   h.off_state_end = A.size;
   // 0xff-initialised (-1) state
   h.off_ff_begin = align_up(A.size, 256);
@@ -467,7 +468,8 @@ void fill_descriptors(nx_sim& h) {
   // longest-expected replicas first: more requests and lower rates run longer
   h.order.resize(h.n_rep);
   std::iota(h.order.begin(), h.order.end(), 0);
-  std::vector<double> cost(h.n_rep);
+  std::vector<double>& cost = h.cost;
+  cost.assign(h.n_rep, 0.0);
   for (int r = 0; r < h.n_rep; ++r) {
     const auto& w = h.wl[r];
     const double span = w.arrival_ms.empty() ? 0.0 : w.arrival_ms.back();
@@ -598,8 +600,25 @@ int nx_sim_launch(nx_sim_t h) {
     const int need = h->n_rep;
     const int grid = std::max(1, std::min(need, per_sm * sm_count(h->device)));
     cuda_check(cudaEventRecord(h->ev0, st), "event");
+    // exclusive SMs: the replicas within 10% of the longest expected cost,
+    // when the batch is skewed (longest > 1.5x mean) and fills 2 CTAs on
+    // every SM; at most a quarter of the SMs
+    int n_excl = 0;
+    const int sms = sm_count(h->device);
+    if (per_sm >= 2 && grid >= 2 * sms && h->n_rep > 1) {
+      double mx = 0.0, sum = 0.0;
+      for (double c : h->cost) {
+        mx = std::max(mx, c);
+        sum += c;
+      }
+      if (mx > 1.5 * sum / h->n_rep)
+        for (int i = 0; i < h->n_rep && h->cost[h->order[i]] >= 0.9 * mx; ++i) ++n_excl;
+      n_excl = std::min(n_excl, sms / 4);
+    }
+    if (const char* ex = std::getenv("NX_EXCL_SMS")) n_excl = std::max(0, std::min(std::atoi(ex), sms / 2));
+    n_excl = std::min(n_excl, h->n_rep);
     cuda_check(nx_launch_sim(h->d_pools, h->d_order, h->n_rep, h->d_next, spw, h->prefix_cap, h->max_eng, grid,
-                             kWarpsPerBlock, st), "nx_sim_kernel launch");
+                             kWarpsPerBlock, n_excl, st), "nx_sim_kernel launch");
     cuda_check(cudaEventRecord(h->ev1, st), "event");
     h->launched = true;
   });

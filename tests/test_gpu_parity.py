@@ -203,3 +203,19 @@ def test_smoke_entry_point():
     sys.path.insert(0, str(ROOT))
     import __graft_entry__
     __graft_entry__.smoke()
+
+
+def test_exclusive_sm_schedule_gives_identical_results(all_cases, monkeypatch):
+    """The kernel's replica scheduling (exclusive SMs for the longest
+    replicas, then the shared queue) changes only where replicas run."""
+    from paper_2509_23384_b200 import sim
+    names = sorted(all_cases)
+    monkeypatch.setenv("NX_EXCL_SMS", "6")
+    b = sim.Batch([all_cases[n] for n in names]).run()
+    try:
+        sums = b.summaries()
+        for i, name in enumerate(names):
+            assert f"{sums[i].event_hash:016x}" == GOLDEN[name]["event_hash"], name
+            assert sums[i].decisions == GOLDEN[name]["decisions"], name
+    finally:
+        b.close()

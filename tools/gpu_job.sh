@@ -1,2 +1,6 @@
 mkdir -p gpurun_out
-timeout 600 python -m pytest tests/test_k6_gpu.py -q > gpurun_out/pytest_k6.txt 2>&1; echo "rc=$?" >> gpurun_out/pytest_k6.txt
+rm -f gpurun_out/excl.txt
+for k in 48 64 24 48 64 32; do
+  echo "== excl $k" >> gpurun_out/excl.txt
+  NX_EXCL_SMS=$k timeout 300 python bench.py --no-cpu-baseline --no-e2e --no-operators >> gpurun_out/excl.txt 2>&1
+done

@@ -43,7 +43,7 @@ struct TeamTask {
 };
 
 // Doubles of one warp's learner scratch for long_window W (nx_learner.cuh
-// layout; host: capi.cpp fill_descriptors allocates kSimWarps per replica).
+// layout; host: capi.cpp fill_descriptors allocates two per replica).
 __host__ __device__ __forceinline__ int64_t refit_scratch_stride(int64_t W) {
   return (10 * W + kFbTable + 5120 + 64 + 31) / 32 * 32;
 }

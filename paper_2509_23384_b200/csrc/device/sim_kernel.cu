@@ -616,7 +616,7 @@ __device__ NX_COLD void step_complete(Ctx& c, int e, int64_t now_us) {
   }
   __syncwarp();
   if (n_fin) tradeoff_refit(c, e);
-  if (c.lane == 0) c.rs->cycles[3] += nx_clock() - t_cs;
+  if (nx_timers_on && c.lane == 0) c.rs->cycles[3] += nx_clock() - t_cs;
   try_begin_step(c, e, now_us);
 }
 
@@ -998,7 +998,7 @@ __device__ void run_replica(Ctx& c) {
                                    static_cast<uint64_t>(rid));
       c.rs->ev_hash = h;
       c.rs->events += 1;
-      c.rs->cycles[0] += nx_clock() - t_sel;
+      if (nx_timers_on) c.rs->cycles[0] += nx_clock() - t_sel;
     }
     __syncwarp();
     switch (kind) {
@@ -1221,7 +1221,9 @@ nx_sim_kernel(const NxPools* __restrict__ pools, const int32_t* __restrict__ ord
     c.log_flags = c.d->log_flags;
     c.roff = c.d->req_off;
     c.soff = c.d->sess_off;
-    c.scratch = pools->scratch + c.d->scratch_off + warp * refit_scratch_stride(c.d->long_w);
+    // learner scratch: the event loop (linear refits) and the refit leader;
+    // helpers only read the leader's staged window
+    c.scratch = pools->scratch + c.d->scratch_off + (warp == 0 ? 0 : 1) * refit_scratch_stride(c.d->long_w);
     c.lin_rows = c.scratch + 6 * c.d->long_w + kFbTable;
     if (warp == 0) init_replica(c);
     __syncthreads();

@@ -301,8 +301,9 @@ void fill_descriptors(nx_sim& h) {
     h.n_learn_log += d.learn_log_cap;
     req_off += n;
     sess_off += ns;
-    // one learner scratch per warp (nx_state.cuh refit_scratch_stride)
-    scratch_off += kWarpsPerBlock * ((10 * static_cast<int64_t>(c.long_window) + 1024 + 5120 + 64 + 31) / 32 * 32);
+    // learner scratch for the event-loop warp and the refit leader
+    // (nx_state.cuh refit_scratch_stride)
+    scratch_off += 2 * ((10 * static_cast<int64_t>(c.long_window) + 1024 + 5120 + 64 + 31) / 32 * 32);
     for (const auto& ec : c.engines) {
       NxEngineDesc e;
       std::memset(&e, 0, sizeof e);

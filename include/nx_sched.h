@@ -31,7 +31,8 @@ const char* nx_last_error(void);
 /* sizeof of the ABI structs, in declaration order (nx_lens_problem,
  * nx_lens_plan, nx_route_group, nx_engine_report, nx_route_request,
  * nx_route_decision, nx_refit_problem, nx_refit_result, nx_replica_summary,
- * nx_request_record) — lets bindings verify their layouts. */
+ * nx_request_record, nx_baseline_problem) — lets bindings verify their
+ * layouts. */
 int nx_abi_sizes(int64_t* out, int32_t n);
 int nx_device_count(void);
 
@@ -252,6 +253,29 @@ int nx_allocate_tokens_host(nx_allocate_problem* p, int32_t n, const int32_t* wa
 int nx_router_scores_host(nx_score_query* q, int32_t n);
 int nx_tradeoff_update_host(nx_tradeoff_state* st, int32_t n, const nx_completion* completions,
                             int64_t n_completions);
+
+/* schedule_baseline (proj/include/servesim/engine.h:68-79,
+ * proj/src/engine.cpp:61-108): the prefill_priority and static_chunked engine
+ * policies. Plan = the first n_decode runners (one decode token each), then
+ * waiters k < n_prefill with tokens[wait_off + k]. Status: NX_ERUNTIME when
+ * prefill_priority cannot fit the first prompt (the reference's
+ * runtime_error), NX_ELOGIC for the lens policy, NX_EINVAL for an
+ * allocate_tokens or predict_latency argument error. */
+enum { NX_SCHED_LENS = 0, NX_SCHED_PREFILL_PRIORITY = 1, NX_SCHED_STATIC_CHUNKED = 2 };
+typedef struct nx_baseline_problem {
+  double params[8];                   /* learner's PerfParams */
+  int64_t m_max, q_max, static_budget;
+  int64_t wait_off;                   /* waiters' remaining prompts at [wait_off, +n_wait) */
+  int32_t policy, engine_id;
+  int32_t n_run, n_wait;
+  int64_t b, s;                       /* out */
+  double predicted_ms;                /* out */
+  int32_t n_decode, n_prefill;        /* out */
+  int32_t status, pad_;               /* out */
+} nx_baseline_problem;
+
+int nx_baseline_schedule_host(nx_baseline_problem* p, int32_t n, const int32_t* wait_remaining,
+                              int64_t n_wait_total, int32_t* tokens);
 
 /* ---- K5 (+K2/K3/K4 inside): batched replica simulation --------------------
  * Replaces servesim::run_simulation / sweep (proj/include/servesim/sim.h:

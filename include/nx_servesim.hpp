@@ -369,6 +369,87 @@ class OnlineLearner {
 
 std::vector<LatencySample> load_samples_jsonl(const std::string& path);
 
+// ---- engine simulator (engine.h:68-180) ---------------------------------------------
+// Host bookkeeping (queues, KV block counters, prefix cache) as in the
+// reference; every scheduling decision, latency prediction, learner refit and
+// tradeoff refit it makes is a device launch (schedule_step /
+// nx_baseline_schedule_host / predict_latency / OnlineLearner /
+// TradeoffEstimator). Inside simulations the same logic runs on the device
+// (sim_kernel.cu); this class serves step-by-step callers.
+struct StepOutcome {
+  BatchPlan plan;
+  double actual_ms = 0.0;
+  std::vector<uint64_t> finished;
+  std::vector<uint64_t> first_tokens;
+};
+
+BatchPlan schedule_baseline(SchedulerPolicy policy, std::span<const Request* const> wait_q,
+                            std::span<const Request* const> run_q, const PerfParams& params,
+                            const EngineConfig& cfg);
+
+class EngineSim {
+ public:
+  EngineSim(const EngineConfig& cfg, const SLOSpec& slo, const SchedulerConfig& sched,
+            const TradeoffModel& tradeoff_init, const LearnerConfig& learner_cfg, uint64_t root_seed);
+
+  double oracle_latency(const BatchShape& shape);
+  bool admit(Request* request, double now_ms);
+  bool busy() const { return step_.has_value(); }
+  bool has_work() const { return !wait_q_.empty() || !run_q_.empty(); }
+  std::optional<double> begin_step(double now_ms);
+  StepOutcome complete_step(double now_ms);
+  StateVector export_state(double now_ms) const;
+  int64_t queue_len() const { return static_cast<int64_t>(wait_q_.size() + run_q_.size()); }
+  void record_learner_sample(const LatencySample& sample) { learner_.record_sample(sample); }
+
+  const EngineConfig& config() const { return cfg_; }
+  const SchedulerConfig& scheduler_config() const { return sched_; }
+  OnlineLearner& learner() { return learner_; }
+  const OnlineLearner& learner() const { return learner_; }
+  TradeoffEstimator& tradeoff() { return tradeoff_; }
+  const BatchPlan* inflight_plan() const { return step_ ? &step_->plan : nullptr; }
+
+  int64_t used_blocks() const { return pinned_; }
+  int64_t free_blocks() const { return cfg_.kv_blocks - pinned_; }
+  int64_t reserved_blocks() const { return reserved_; }
+  int64_t cache_blocks() const { return cached_; }
+  int64_t cached_prefix_tokens(const std::string& session) const;
+  void check_kv_consistency() const;
+
+  const std::deque<Request*>& wait_queue() const { return wait_q_; }
+  const std::vector<Request*>& run_queue() const { return run_q_; }
+
+ private:
+  struct Step {
+    BatchPlan plan;
+    double started_ms = 0.0, actual_ms = 0.0;
+  };
+  struct Prefix {  // a finished session's KV prefix, kept in free space
+    int64_t tokens = 0, blocks = 0;
+    uint64_t stamp = 0;  // insertion order; the smallest stamp is evicted first
+  };
+  int64_t blocks(int64_t tokens) const { return (tokens + cfg_.block_size - 1) / cfg_.block_size; }
+  void drop_prefix(std::unordered_map<std::string, Prefix>::iterator it);
+  void shrink_cache();
+  void keep_prefix(const std::string& session, int64_t tokens);
+  void admit_prefills(BatchPlan& plan);
+
+  EngineConfig cfg_;
+  SLOSpec slo_;
+  SchedulerConfig sched_;
+  OnlineLearner learner_;
+  TradeoffEstimator tradeoff_;
+  Rng noise_;
+  std::deque<Request*> wait_q_;
+  std::vector<Request*> run_q_;
+  std::unordered_map<uint64_t, Request*> live_;
+  std::optional<Step> step_;
+  int64_t pinned_ = 0, reserved_ = 0, cached_ = 0;
+  std::unordered_map<std::string, Prefix> prefixes_;
+  std::map<uint64_t, std::string> lru_;  // stamp -> session
+  uint64_t next_stamp_ = 0;
+};
+
 // ---- metrics (metrics.h) ---------------------------------------------------------------
 struct RequestRecord {
   uint64_t request_id = 0;

@@ -283,6 +283,55 @@ int ref_schedule_step(const int64_t* w_prompt, const int64_t* w_prefilled,
   }
 }
 
+// schedule_baseline over explicit queues (ids as in ref_schedule_step).
+// Output: b, s, predicted, and allocations (id, tokens, prefill).
+int ref_schedule_baseline(int policy, const int64_t* w_prompt, const int64_t* w_prefilled,
+                          int64_t n_wait, int64_t n_run, const double* params8, int64_t m_max,
+                          int64_t q_max, int64_t static_budget, int engine_id, int64_t* out_bs,
+                          double* out_pred, int64_t* alloc_id, int64_t* alloc_tokens,
+                          int* alloc_prefill) {
+  try {
+    std::vector<Request> store(static_cast<size_t>(n_wait + n_run));
+    std::vector<const Request*> wait, run;
+    for (int64_t i = 0; i < n_run; ++i) {
+      Request& r = store[i];
+      r.id = static_cast<uint64_t>(i);
+      r.prompt_len = 64;
+      r.prefilled = 64;
+      r.state = RequestState::kRunning;
+      run.push_back(&r);
+    }
+    for (int64_t i = 0; i < n_wait; ++i) {
+      Request& r = store[n_run + i];
+      r.id = static_cast<uint64_t>(1000 + i);
+      r.prompt_len = w_prompt[i];
+      r.prefilled = w_prefilled[i];
+      wait.push_back(&r);
+    }
+    EngineConfig cfg;
+    cfg.engine_id = engine_id;
+    cfg.m_max = m_max;
+    cfg.q_max = q_max;
+    cfg.static_budget = static_budget;
+    const SchedulerPolicy pol = policy == 1   ? SchedulerPolicy::kPrefillPriority
+                                : policy == 2 ? SchedulerPolicy::kStaticChunked
+                                              : SchedulerPolicy::kLens;
+    const BatchPlan plan = schedule_baseline(pol, wait, run, params_from(params8), cfg);
+    out_bs[0] = plan.b;
+    out_bs[1] = plan.s;
+    *out_pred = plan.predicted_ms;
+    for (size_t i = 0; i < plan.allocations.size(); ++i) {
+      alloc_id[i] = static_cast<int64_t>(plan.allocations[i].request_id);
+      alloc_tokens[i] = plan.allocations[i].tokens;
+      alloc_prefill[i] = plan.allocations[i].is_prefill;
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return classify(e);
+  }
+}
+
 // PRISM route over a report table. state rows: l_hat, w_load, m_free, p_max,
 // reported_at (5 doubles) + queue_len + has_report. Session affinity is given
 // by `affine_engine` (engine id previously completing this session, or -1).

@@ -48,14 +48,21 @@ REFIT_PROBLEM = np.dtype([
 REFIT_RESULT = np.dtype([("params", "f8", 8), ("counters", "i8", 7), ("updated", "i4"),
                          ("status", "i4")], align=True)
 
-ORDER = [LENS_PROBLEM, LENS_PLAN, ROUTE_GROUP, ENGINE_REPORT, ROUTE_REQUEST, ROUTE_DECISION,
-         REFIT_PROBLEM, REFIT_RESULT]
+BASELINE_PROBLEM = np.dtype([
+    ("params", "f8", 8), ("m_max", "i8"), ("q_max", "i8"), ("static_budget", "i8"),
+    ("wait_off", "i8"), ("policy", "i4"), ("engine_id", "i4"), ("n_run", "i4"), ("n_wait", "i4"),
+    ("b", "i8"), ("s", "i8"), ("predicted_ms", "f8"), ("n_decode", "i4"), ("n_prefill", "i4"),
+    ("status", "i4"), ("pad_", "i4")], align=True)
+
+# position in nx_abi_sizes' list -> layout (8, 9: replica summary / request record)
+ORDER = {0: LENS_PROBLEM, 1: LENS_PLAN, 2: ROUTE_GROUP, 3: ENGINE_REPORT, 4: ROUTE_REQUEST,
+         5: ROUTE_DECISION, 6: REFIT_PROBLEM, 7: REFIT_RESULT, 10: BASELINE_PROBLEM}
 
 
 def check_layouts() -> None:
-    out = (C.c_int64 * 10)()
-    lib().nx_abi_sizes(out, 10)
-    for i, dt in enumerate(ORDER):
+    out = (C.c_int64 * 11)()
+    lib().nx_abi_sizes(out, 11)
+    for i, dt in ORDER.items():
         if dt.itemsize != out[i]:
             raise RuntimeError(f"ABI layout mismatch for struct #{i}: numpy {dt.itemsize} vs C {out[i]}")
 

@@ -56,6 +56,28 @@ __global__ void nx_budget_kernel(nx_budget_query* __restrict__ q, int n) {
   r.status = NX_OK;
 }
 
+// Saturating inclusive prefix of the first `slots` waiters' remaining prompts:
+// pr[0] = 0, pr[k + 1] = min(2^30, sum_{i<=k} wr[i]); one warp.
+__device__ void waiter_prefix(const int32_t* wr, int slots, int32_t* pr, int lane) {
+  __syncwarp();
+  if (lane == 0) pr[0] = 0;
+  long long carry = 0;
+  for (int base = 0; base < slots; base += 32) {
+    const int i = base + lane;
+    long long s = i < slots ? wr[i] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long u = __shfl_up_sync(NX_FULL, s, o);
+      if (lane >= o) s += u;
+    }
+    const long long tot = carry + s;
+    if (i < slots) pr[i + 1] = static_cast<int32_t>(tot < (1 << 30) ? tot : (1 << 30));
+    carry += __shfl_sync(NX_FULL, s, 31);
+    if (carry > (1 << 30)) carry = 1 << 30;
+  }
+  __syncwarp();
+}
+
 // allocate_tokens (lens.cpp:58-79), one warp per problem: every waiter takes
 // min(remaining, budget left) while slots remain (the prefix-sum form).
 __global__ void nx_allocate_kernel(nx_allocate_problem* __restrict__ probs, int n,
@@ -86,23 +108,7 @@ __global__ void nx_allocate_kernel(nx_allocate_problem* __restrict__ probs, int 
   }
   // saturating prefix (only compared against budgets < 2^30)
   int32_t* pr = pre[w];
-  __syncwarp();
-  if (lane == 0) pr[0] = 0;
-  long long carry = 0;
-  for (int base = 0; base < slots; base += 32) {
-    const int i = base + lane;
-    long long s = i < slots ? wr[i] : 0;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const long long u = __shfl_up_sync(NX_FULL, s, o);
-      if (lane >= o) s += u;
-    }
-    const long long tot = carry + s;
-    if (i < slots) pr[i + 1] = static_cast<int32_t>(tot < (1 << 30) ? tot : (1 << 30));
-    carry += __shfl_sync(NX_FULL, s, 31);
-    if (carry > (1 << 30)) carry = 1 << 30;
-  }
-  __syncwarp();
+  waiter_prefix(wr, slots, pr, lane);
   const int j = budget > 0 ? lens_lower_bound(pr, slots, budget) : 0;
   for (int k = lane; k < j; k += 32) {
     const int rr = pr[k + 1] - pr[k];
@@ -111,6 +117,123 @@ __global__ void nx_allocate_kernel(nx_allocate_problem* __restrict__ probs, int 
   }
   if (lane == 0) {
     p.n_prefill = j;
+    p.status = NX_OK;
+  }
+}
+
+// schedule_baseline (engine.cpp:61-108), one warp per problem.
+//  prefill_priority: whole remaining prompts, FCFS, while the batch stays
+//    within q_max requests and m_max tokens (k waiters fit iff k <= q_max and
+//    prefix[k] <= m_max); with nobody waiting, every runner decodes.
+//  static_chunked: allocate_tokens(run, wait, b, s) with b = min(|run| +
+//    |wait|, q_max), s = min(m_max, max(static_budget, b)).
+__global__ void nx_baseline_kernel(nx_baseline_problem* __restrict__ probs, int n,
+                                   const int32_t* __restrict__ rem, int32_t* __restrict__ tokens) {
+  __shared__ int32_t pre[4][1025];
+  const int lane = lane_id(), w = threadIdx.x >> 5;
+  const int pi = blockIdx.x * 4 + w;
+  if (pi >= n) return;
+  nx_baseline_problem& p = probs[pi];
+  auto finish = [&](int status) {
+    if (lane == 0) p.status = status;
+  };
+  if (lane == 0) {
+    p.b = 0;
+    p.s = 0;
+    p.predicted_ms = 0.0;
+    p.n_decode = 0;
+    p.n_prefill = 0;
+  }
+  if (p.policy != NX_SCHED_PREFILL_PRIORITY && p.policy != NX_SCHED_STATIC_CHUNKED) {
+    finish(p.policy == NX_SCHED_LENS ? NX_ELOGIC : NX_EINVAL);
+    return;
+  }
+  const int R = p.n_run, W = p.n_wait;
+  if (R == 0 && W == 0) {
+    finish(NX_OK);  // empty plan, no prediction
+    return;
+  }
+  const int32_t* wr = rem + p.wait_off;
+  int32_t* pr = pre[w];
+  int64_t b = 0, s = 0;
+  int n_dec = 0, j = 0;
+  if (p.policy == NX_SCHED_PREFILL_PRIORITY) {
+    if (W > 0) {
+      const int64_t cap = p.q_max < W ? p.q_max : W;
+      if (cap > 1024 || p.m_max >= (int64_t(1) << 30)) {
+        finish(NX_EINVAL);  // device limit
+        return;
+      }
+      const int slots = static_cast<int>(cap);
+      bool bad = false;
+      for (int i = lane; i < slots; i += 32) bad |= wr[i] < 1;
+      if (__any_sync(NX_FULL, bad)) {
+        finish(NX_EINVAL);  // device limit: remaining prompt >= 1
+        return;
+      }
+      waiter_prefix(wr, slots, pr, lane);
+      j = lens_lower_bound(pr + 1, slots, static_cast<int>(p.m_max) + 1);
+      if (j == 0) {
+        finish(NX_ERUNTIME);  // prompt exceeds m_max
+        return;
+      }
+      b = j;
+      s = pr[j];
+      for (int k = lane; k < j; k += 32) tokens[p.wait_off + k] = wr[k];
+    } else {
+      n_dec = R;
+      b = R;
+      s = R;
+    }
+  } else {
+    const int64_t tot = static_cast<int64_t>(R) + W;
+    const int64_t bb = tot < p.q_max ? tot : p.q_max;
+    const int64_t sb = p.static_budget < bb ? bb : p.static_budget;
+    const int64_t ss = p.m_max < sb ? p.m_max : sb;
+    if (bb < R || ss < bb) {
+      finish(NX_EINVAL);  // allocate_tokens: budget below queue needs
+      return;
+    }
+    const int64_t slots64 = bb - R < W ? bb - R : W;
+    const int64_t budget64 = ss - R;
+    if (slots64 > 1024 || budget64 >= (int64_t(1) << 30)) {
+      finish(NX_EINVAL);  // device limit
+      return;
+    }
+    const int slots = static_cast<int>(slots64), budget = static_cast<int>(budget64);
+    bool bad = false;
+    for (int i = lane; i < slots; i += 32) bad |= wr[i] < 1;
+    if (__any_sync(NX_FULL, bad)) {
+      finish(NX_EINVAL);
+      return;
+    }
+    waiter_prefix(wr, slots, pr, lane);
+    j = budget > 0 ? lens_lower_bound(pr, slots, budget) : 0;
+    int64_t got = 0;
+    for (int k = lane; k < j; k += 32) {
+      const int rr = pr[k + 1] - pr[k];
+      const int left = budget - pr[k];
+      const int t = rr < left ? rr : left;
+      tokens[p.wait_off + k] = t;
+      got += t;
+    }
+    for (int o = 16; o > 0; o >>= 1) got += __shfl_xor_sync(NX_FULL, got, o);
+    n_dec = R;
+    b = static_cast<int64_t>(R) + j;
+    s = static_cast<int64_t>(R) + got;
+  }
+  // predict_latency(params, {b, s}) (perf_model.cpp:22-49)
+  const Params P = params_from(p.params);
+  if (!params_valid(P)) {
+    finish(NX_EINVAL);
+    return;
+  }
+  if (lane == 0) {
+    p.b = b;
+    p.s = s;
+    p.n_decode = n_dec;
+    p.n_prefill = j;
+    p.predicted_ms = predict(P, static_cast<double>(b), static_cast<double>(s));
     p.status = NX_OK;
   }
 }
@@ -226,6 +349,11 @@ extern "C" cudaError_t nx_launch_scalar_ops(int op, void* recs, int n, const voi
     case 4:
       nx_tradeoff_kernel<<<(n + 3) / 4, 128, 0, st>>>(static_cast<nx_tradeoff_state*>(recs), n,
                                                       static_cast<const nx_completion*>(aux_in));
+      break;
+    case 5:
+      nx_baseline_kernel<<<(n + 3) / 4, 128, 0, st>>>(static_cast<nx_baseline_problem*>(recs), n,
+                                                      static_cast<const int32_t*>(aux_in),
+                                                      static_cast<int32_t*>(aux_out));
       break;
     default:
       return cudaErrorInvalidValue;

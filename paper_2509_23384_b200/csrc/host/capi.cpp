@@ -1007,7 +1007,7 @@ int nx_abi_sizes(int64_t* out, int32_t n) {
   const int64_t sz[] = {sizeof(nx_lens_problem), sizeof(nx_lens_plan), sizeof(nx_route_group),
                         sizeof(nx_engine_report), sizeof(nx_route_request), sizeof(nx_route_decision),
                         sizeof(nx_refit_problem), sizeof(nx_refit_result), sizeof(nx_replica_summary),
-                        sizeof(nx_request_record)};
+                        sizeof(nx_request_record), sizeof(nx_baseline_problem)};
   for (int32_t i = 0; i < n && i < static_cast<int32_t>(sizeof sz / sizeof sz[0]); ++i) out[i] = sz[i];
   return NX_OK;
 }
@@ -1241,6 +1241,19 @@ int nx_allocate_tokens_host(nx_allocate_problem* p, int32_t n, const int32_t* wa
     run_scalar_op(2, p, sizeof *p, n, wait_remaining, sizeof(int32_t) * n_wait_total, tokens,
                   sizeof(int32_t) * n_wait_total);
     first_status(p, n, "allocate_tokens");
+  });
+}
+
+int nx_baseline_schedule_host(nx_baseline_problem* p, int32_t n, const int32_t* wait_remaining,
+                              int64_t n_wait_total, int32_t* tokens) {
+  return guard([&] {
+    if (n <= 0) return;
+    for (int32_t i = 0; i < n; ++i)
+      if (p[i].n_run < 0 || p[i].n_wait < 0 || p[i].wait_off < 0 || p[i].wait_off + p[i].n_wait > n_wait_total)
+        throw std::invalid_argument("schedule_baseline: queue range out of bounds");
+    run_scalar_op(5, p, sizeof *p, n, wait_remaining, sizeof(int32_t) * n_wait_total, tokens,
+                  sizeof(int32_t) * n_wait_total);
+    first_status(p, n, "schedule_baseline");
   });
 }
 

@@ -590,6 +590,238 @@ std::string to_string(SchedulerPolicy policy) {
   return "?";
 }
 
+// ---- engine simulator (engine.cpp) ---------------------------------------------------
+BatchPlan schedule_baseline(SchedulerPolicy policy, std::span<const Request* const> wait_q,
+                            std::span<const Request* const> run_q, const PerfParams& params,
+                            const EngineConfig& cfg) {
+  nx_baseline_problem p{};
+  pack(params, p.params);
+  p.m_max = cfg.m_max;
+  p.q_max = cfg.q_max;
+  p.static_budget = cfg.static_budget;
+  p.policy = policy == SchedulerPolicy::kPrefillPriority ? NX_SCHED_PREFILL_PRIORITY
+             : policy == SchedulerPolicy::kStaticChunked ? NX_SCHED_STATIC_CHUNKED
+                                                         : NX_SCHED_LENS;
+  p.engine_id = cfg.engine_id;
+  p.n_run = to_i32(static_cast<int64_t>(run_q.size()), "schedule_baseline");
+  p.n_wait = to_i32(static_cast<int64_t>(wait_q.size()), "schedule_baseline");
+  std::vector<int32_t> rem(wait_q.size()), tok(wait_q.size(), 0);
+  for (size_t i = 0; i < wait_q.size(); ++i) rem[i] = to_i32(wait_q[i]->remaining_prompt(), "remaining prompt");
+  const int rc = nx_baseline_schedule_host(&p, 1, rem.data(), static_cast<int64_t>(rem.size()), tok.data());
+  if (rc == NX_ERUNTIME && p.status == NX_ERUNTIME)
+    throw std::runtime_error("prefill_priority: prompt exceeds m_max; raise m_max for engine " +
+                             std::to_string(cfg.engine_id));
+  if (rc == NX_ELOGIC && p.status == NX_ELOGIC) throw std::logic_error("schedule_baseline called with lens policy");
+  raise(rc);
+  BatchPlan out;
+  out.b = p.b;
+  out.s = p.s;
+  out.predicted_ms = p.predicted_ms;
+  out.allocations.reserve(static_cast<size_t>(p.n_decode + p.n_prefill));
+  for (int32_t i = 0; i < p.n_decode; ++i) out.allocations.push_back({run_q[i]->id, 1, false});
+  for (int32_t k = 0; k < p.n_prefill; ++k) out.allocations.push_back({wait_q[k]->id, tok[k], true});
+  return out;
+}
+
+EngineSim::EngineSim(const EngineConfig& cfg, const SLOSpec& slo, const SchedulerConfig& sched,
+                     const TradeoffModel& tradeoff_init, const LearnerConfig& learner_cfg, uint64_t root_seed)
+    : cfg_(cfg),
+      slo_(slo),
+      sched_(sched),
+      learner_(OnlineLearner::default_priors(), learner_cfg),
+      tradeoff_(tradeoff_init),
+      noise_(substream_seed(root_seed, "engine-noise", static_cast<uint64_t>(cfg.engine_id))) {
+  if (!cfg_.valid()) throw std::invalid_argument("invalid EngineConfig");
+  sched_.m_max = cfg_.m_max;  // the engine's own batch caps win (engine.cpp:122-124)
+  sched_.q_max = cfg_.q_max;
+  if (!sched_.valid()) throw std::invalid_argument("invalid SchedulerConfig");
+}
+
+// Ground truth T_true(shape) * exp(sigma z) on the engine's noise stream
+// (engine.cpp:128-132); T_true is a K1 launch.
+double EngineSim::oracle_latency(const BatchShape& shape) {
+  const double t = predict_latency(cfg_.true_params, shape);
+  return cfg_.noise_sigma == 0.0 ? t : t * std::exp(cfg_.noise_sigma * noise_.normal());
+}
+
+int64_t EngineSim::cached_prefix_tokens(const std::string& session) const {
+  const auto it = prefixes_.find(session);
+  return it == prefixes_.end() ? 0 : it->second.tokens;
+}
+
+void EngineSim::drop_prefix(std::unordered_map<std::string, Prefix>::iterator it) {
+  cached_ -= it->second.blocks;
+  lru_.erase(it->second.stamp);
+  prefixes_.erase(it);
+}
+
+// Reclaim least-recently-finished prefixes until the cache fits the free
+// blocks (engine.cpp:285-292).
+void EngineSim::shrink_cache() {
+  while (cached_ > free_blocks() && !lru_.empty()) drop_prefix(prefixes_.find(lru_.begin()->second));
+}
+
+void EngineSim::keep_prefix(const std::string& session, int64_t tokens) {
+  if (const auto it = prefixes_.find(session); it != prefixes_.end()) drop_prefix(it);
+  const uint64_t stamp = next_stamp_++;
+  prefixes_[session] = Prefix{tokens, blocks(tokens), stamp};
+  lru_.emplace(stamp, session);
+  cached_ += blocks(tokens);
+  shrink_cache();
+}
+
+// admit (engine.cpp:139-169): a cached prefix of the session credits up to
+// prompt - 1 tokens when its blocks fit beside the committed ones.
+bool EngineSim::admit(Request* request, double now_ms) {
+  (void)now_ms;
+  if (request->state != RequestState::kWaiting) throw std::invalid_argument("admit: request not in waiting state");
+  if (cfg_.wait_cap > 0 && static_cast<int64_t>(wait_q_.size()) >= cfg_.wait_cap) return false;
+  if (const auto it = prefixes_.find(request->session_id); it != prefixes_.end()) {
+    const int64_t credit = std::min(it->second.tokens, request->prompt_len - 1);
+    const int64_t need = blocks(credit);
+    if (credit > 0 && pinned_ + reserved_ + need <= cfg_.kv_blocks) {
+      drop_prefix(it);
+      request->prefilled = credit;
+      request->precredited = credit;
+      pinned_ += need;
+    }
+  }
+  wait_q_.push_back(request);
+  live_[request->id] = request;
+  return true;
+}
+
+// trim_for_kv (engine.cpp:185-213): a waiter's first prefill reserves its
+// whole footprint; the first one that does not fit ends the admissible FCFS
+// prefix of new prefills (decodes and already-admitted prefills stay).
+void EngineSim::admit_prefills(BatchPlan& plan) {
+  std::vector<Allocation> keep;
+  keep.reserve(plan.allocations.size());
+  bool full = false;
+  for (const Allocation& a : plan.allocations) {
+    Request* r = live_.at(a.request_id);
+    if (!a.is_prefill || r->kv_admitted) {
+      keep.push_back(a);
+      continue;
+    }
+    if (full) continue;
+    const int64_t grow = blocks(r->prompt_len + r->target_decode) - blocks(r->prefilled + r->decoded);
+    if (pinned_ + reserved_ + grow > cfg_.kv_blocks) {
+      full = true;
+      continue;
+    }
+    reserved_ += grow;
+    r->kv_admitted = true;
+    keep.push_back(a);
+  }
+  if (keep.size() == plan.allocations.size()) return;
+  plan.allocations = std::move(keep);
+  plan.b = static_cast<int64_t>(plan.allocations.size());
+  plan.s = 0;
+  for (const Allocation& a : plan.allocations) plan.s += a.tokens;
+  plan.predicted_ms = plan.b > 0 ? predict_latency(learner_.params(), {plan.b, plan.s}) : 0.0;
+}
+
+std::optional<double> EngineSim::begin_step(double now_ms) {
+  if (busy()) throw std::logic_error("begin_step on a busy engine");
+  if (!has_work()) return std::nullopt;
+  const std::vector<const Request*> run(run_q_.begin(), run_q_.end());
+  const std::vector<const Request*> wait(wait_q_.begin(), wait_q_.end());
+  BatchPlan plan = cfg_.scheduler_policy == SchedulerPolicy::kLens
+                       ? schedule_step(wait, run, slo_, tradeoff_.model(), learner_.params(), sched_)
+                       : schedule_baseline(cfg_.scheduler_policy, wait, run, learner_.params(), cfg_);
+  if (plan.empty()) return std::nullopt;
+  admit_prefills(plan);
+  if (plan.empty()) return std::nullopt;
+  const double actual = oracle_latency({plan.b, plan.s});
+  step_ = Step{std::move(plan), now_ms, actual};
+  return actual;
+}
+
+// complete_step (engine.cpp:226-283): token and block accounting per
+// allocation, first-token / finish transitions, prefix caching of finished
+// sessions, then one tradeoff refit over this step's completions.
+StepOutcome EngineSim::complete_step(double now_ms) {
+  if (!busy()) throw std::logic_error("complete_step on an idle engine");
+  StepOutcome out;
+  out.plan = std::move(step_->plan);
+  out.actual_ms = step_->actual_ms;
+  step_.reset();
+  std::vector<CompletionStats> done;
+  for (const Allocation& a : out.plan.allocations) {
+    Request* r = live_.at(a.request_id);
+    const int64_t before = blocks(r->prefilled + r->decoded);
+    if (a.is_prefill) {
+      r->prefilled += a.tokens;
+      r->allocated_prefill += a.tokens;
+    } else {
+      r->decoded += 1;
+      r->allocated_decode += 1;
+    }
+    const int64_t grew = blocks(r->prefilled + r->decoded) - before;
+    pinned_ += grew;
+    reserved_ -= grew;
+    if (a.is_prefill) {
+      if (r->prefilled != r->prompt_len) continue;
+      r->state = RequestState::kRunning;
+      r->first_token_ms = now_ms;
+      out.first_tokens.push_back(r->id);
+      wait_q_.erase(std::find(wait_q_.begin(), wait_q_.end(), r));
+      run_q_.push_back(r);
+    } else if (r->decoded == r->target_decode) {
+      r->state = RequestState::kFinished;
+      out.finished.push_back(r->id);
+      CompletionStats c;
+      c.ttft_ms = *r->first_token_ms - r->arrival_ms;
+      c.decode_len = r->target_decode;
+      c.tpot_ms = r->target_decode >= 2
+                      ? (now_ms - *r->first_token_ms) / static_cast<double>(r->target_decode - 1)
+                      : 0.0;
+      done.push_back(c);
+      pinned_ -= blocks(r->prefilled + r->decoded);
+      keep_prefix(r->session_id, r->prefilled + r->decoded);
+      run_q_.erase(std::find(run_q_.begin(), run_q_.end(), r));
+      live_.erase(r->id);
+    }
+  }
+  shrink_cache();
+  if (!done.empty()) tradeoff_.update(done);
+  return out;
+}
+
+// export_state (engine.cpp:307-332).
+StateVector EngineSim::export_state(double now_ms) const {
+  StateVector v;
+  v.engine_id = cfg_.engine_id;
+  v.reported_at_ms = now_ms;
+  v.p_max = learner_.params().p_max;
+  if (step_) v.l_hat_ms = std::max(0.0, step_->plan.predicted_ms - (now_ms - step_->started_ms));
+  const double l_bar = tradeoff_.model().l_bar;
+  double prefill = 0.0, demand = 0.0;
+  for (const Request* r : wait_q_) {
+    const double left = static_cast<double>(r->remaining_prompt());
+    prefill += left;
+    demand += left + l_bar;
+  }
+  v.w_load_tokens = prefill + 32.0 * static_cast<double>(wait_q_.size() + run_q_.size());
+  v.m_free_tokens = std::max(0.0, static_cast<double>(free_blocks() * cfg_.block_size) - demand);
+  return v;
+}
+
+// check_kv_consistency (engine.cpp:334-361).
+void EngineSim::check_kv_consistency() const {
+  int64_t held = 0;
+  for (const auto& kv : live_) held += blocks(kv.second->prefilled + kv.second->decoded);
+  if (held != pinned_) throw std::logic_error("kv accounting drift: pinned mismatch");
+  if (pinned_ + free_blocks() != cfg_.kv_blocks) throw std::logic_error("kv conservation violated");
+  if (pinned_ < 0 || reserved_ < 0 || cached_ < 0) throw std::logic_error("negative kv counter");
+  if (pinned_ + reserved_ > cfg_.kv_blocks) throw std::logic_error("kv oversubscribed");
+  if (cached_ > free_blocks()) throw std::logic_error("prefix cache exceeds free space");
+  int64_t cache = 0;
+  for (const auto& kv : prefixes_) cache += kv.second.blocks;
+  if (cache != cached_) throw std::logic_error("kv accounting drift: cache mismatch");
+}
+
 // ---- metrics ------------------------------------------------------------------------
 namespace {
 nx::RecordRow row_of(const RequestRecord& r) {

@@ -118,6 +118,49 @@ def schedule_batch_device(problems, wait_remaining, plans, alloc_tokens, stream=
                                      plans.data_ptr(), alloc_tokens.data_ptr(), st))
 
 
+# ---- baseline engine policies (engine.h:68-79) -------------------------------------
+PREFILL_PRIORITY, STATIC_CHUNKED = 1, 2   # NX_SCHED_* (SchedulerPolicy order)
+
+
+def baseline_record(policy: int, n_run: int, n_wait: int, wait_off: int, params, m_max: int = 8192,
+                    q_max: int = 256, static_budget: int = 2048, engine_id: int = 0) -> np.ndarray:
+    """One nx_baseline_problem record (policy 0 = lens is a logic error)."""
+    r = np.zeros((), dtype=abi.BASELINE_PROBLEM)
+    r["params"] = _row(params)
+    r["m_max"], r["q_max"], r["static_budget"] = m_max, q_max, static_budget
+    r["policy"], r["engine_id"] = policy, engine_id
+    r["n_run"], r["n_wait"], r["wait_off"] = n_run, n_wait, wait_off
+    return r
+
+
+def schedule_baseline_batch(problems: np.ndarray, wait_remaining: np.ndarray, raise_errors: bool = True):
+    """Batched schedule_baseline (engine.cpp:61-108) on host arrays. Returns
+    (problems with b/s/predicted_ms/n_decode/n_prefill/status filled,
+    tokens) — tokens[wait_off + k] is waiter k's prefill for k < n_prefill."""
+    probs = np.array(problems, dtype=abi.BASELINE_PROBLEM, copy=True).reshape(-1)
+    rem = np.ascontiguousarray(wait_remaining, dtype=np.int32)
+    tok = np.zeros(rem.size, dtype=np.int32)
+    rc = lib().nx_baseline_schedule_host(abi.ptr(probs), probs.size, abi.ptr(rem), rem.size, abi.ptr(tok))
+    if raise_errors or not (probs["status"] != 0).any():
+        check(rc)
+    return probs, tok
+
+
+def schedule_baseline(policy: int, wait_q, run_q, params, m_max: int = 8192, q_max: int = 256,
+                      static_budget: int = 2048, engine_id: int = 0) -> BatchPlan:
+    """servesim::schedule_baseline (engine.cpp:61-108), one decision on the device."""
+    rem = np.asarray([r.remaining_prompt() for r in wait_q], dtype=np.int64)
+    if rem.size and (rem.min() < 1 or rem.max() >= 2 ** 31):
+        raise ValueError("schedule_baseline: device path needs 1 <= remaining prompt < 2^31")
+    prob = baseline_record(policy, len(run_q), len(wait_q), 0, params, m_max, q_max, static_budget, engine_id)
+    p, tok = schedule_baseline_batch(prob, rem.astype(np.int32))
+    p = p[0]
+    plan = BatchPlan(b=int(p["b"]), s=int(p["s"]), predicted_ms=float(p["predicted_ms"]))
+    plan.allocations = [Allocation(run_q[i].id, 1, False) for i in range(int(p["n_decode"]))]
+    plan.allocations += [Allocation(wait_q[k].id, int(tok[k]), True) for k in range(int(p["n_prefill"]))]
+    return plan
+
+
 def schedule_step(wait_q, run_q, slo: SLOSpec, tm: TradeoffModel, params,
                   cfg: SchedulerConfig) -> BatchPlan:
     """servesim::schedule_step (lens.cpp:96-146), one decision on the device."""

@@ -72,14 +72,23 @@ def main():
             r = {"status": 0, "params": [hx(x) for x in r["params"]], "updated": r["updated"],
                  "counters": r["counters"].tolist()}
         refit_out.append(r)
+    base = ops_cases.baseline_cases()
+    base_out = []
+    for c in base:
+        r = ref.schedule_baseline(c["policy"], c["n_run"], c["prompt"], c["prefilled"], c["params"],
+                                  c["m_max"], c["q_max"], c["static_budget"], c["engine_id"])
+        if r["status"] == 0:
+            r["predicted"] = hx(r["predicted"])
+        base_out.append(r)
     out = {
         "digest": {"lens": digest(lens), "route": digest(routes),
-                   "refit": digest((metas, b, s, y))},
-        "lens": lens_out, "route": route_out, "refit": refit_out,
+                   "refit": digest((metas, b, s, y)), "baseline": digest(base)},
+        "lens": lens_out, "route": route_out, "refit": refit_out, "baseline": base_out,
     }
     (ROOT / "tests" / "golden" / "ops_golden.json").write_text(json.dumps(out))
-    bad = sum(r["status"] != 0 for r in lens_out + route_out + refit_out)
-    print(f"lens {len(lens_out)} route {len(route_out)} refit {len(refit_out)} (error cases {bad})")
+    bad = sum(r["status"] != 0 for r in lens_out + route_out + refit_out + base_out)
+    print(f"lens {len(lens_out)} route {len(route_out)} refit {len(refit_out)} "
+          f"baseline {len(base_out)} (error cases {bad})")
 
 
 if __name__ == "__main__":

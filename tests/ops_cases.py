@@ -82,6 +82,45 @@ def lens_cases():
     return out
 
 
+# ---- schedule_baseline (engine.cpp:61-108) ---------------------------------------
+def _base(policy, n_run, rem, prefilled=None, params=FAST, m_max=8192, q_max=256, static_budget=2048,
+          engine_id=0):
+    rem = [int(x) for x in rem]
+    pre = [0] * len(rem) if prefilled is None else [int(x) for x in prefilled]
+    return {"policy": int(policy), "n_run": int(n_run), "prompt": [r + p for r, p in zip(rem, pre)],
+            "prefilled": pre, "params": [float(x) for x in params], "m_max": int(m_max),
+            "q_max": int(q_max), "static_budget": int(static_budget), "engine_id": int(engine_id)}
+
+
+def baseline_cases():
+    rng = np.random.default_rng(61108)
+    out = []
+    for pol in (1, 2):
+        out.append(_base(pol, 0, []))                                # empty plan
+        out.append(_base(pol, 5, []))                                # decodes only
+        out.append(_base(pol, 5, [300, 400], q_max=64))              # test_engine.cpp:282-352 shapes
+        out.append(_base(pol, 3, [1000], static_budget=512, q_max=64))
+    out.append(_base(1, 0, [9000], m_max=8192, engine_id=7))         # first prompt > m_max: runtime_error
+    out.append(_base(1, 2, [100, 9000, 5], m_max=8192))              # stops at the first misfit
+    out.append(_base(1, 0, [10] * 40, q_max=16))                     # q_max cap
+    out.append(_base(2, 300, [10], q_max=256))                       # |run| > q_max: invalid_argument
+    out.append(_base(0, 1, [10]))                                    # lens policy: logic_error
+    out.append(_base(2, 1, [10], params=[1, 0, 1, 0, 0, 10, -1.0, 0.05]))   # invalid params
+    for _ in range(300):
+        pol = int(rng.integers(1, 3))
+        q = int(rng.integers(1, 300))
+        m = q + int(rng.integers(0, 20000))
+        R = int(rng.integers(0, q + 1))
+        W = int(rng.integers(0, 400))
+        rem = np.exp(rng.uniform(0, math.log(12000), W)).astype(np.int64) + 1
+        pre = rng.integers(0, 64, W)
+        base = [FAST, MEDIUM, SLOW, PRIORS][int(rng.integers(0, 4))]
+        sb = int(rng.integers(1, m + 1))
+        out.append(_base(pol, R, rem, pre, params=_perturb(rng, base), m_max=m, q_max=q,
+                         static_budget=sb, engine_id=int(rng.integers(0, 16))))
+    return out
+
+
 # ---- K3 ------------------------------------------------------------------------
 def _cfg9(rng, weights=None):
     w = weights if weights is not None else [float(rng.choice([0.0, 0.5, 1.0, 1.0, 2.0])) for _ in range(4)]

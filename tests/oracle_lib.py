@@ -88,6 +88,8 @@ class Ref(_Lib):
         L.ref_schedule_step.argtypes = [V, V, C.c_int64, C.c_int64, C.c_double, C.c_double, V, V,
                                         C.c_int64, C.c_int64, C.c_int, C.c_double, C.c_double,
                                         V, V, V, V, V, V]
+        L.ref_schedule_baseline.argtypes = [C.c_int, V, V, C.c_int64, C.c_int64, V, C.c_int64,
+                                            C.c_int64, C.c_int64, C.c_int, V, V, V, V, V]
         L.ref_route_group.argtypes = [C.c_int, V, C.c_double, C.c_double, C.c_uint64, C.c_int, V, V,
                                       V, V, V, C.c_int, V, V, V, C.c_int, V, V, V, V, V, V, V, V, V]
         L.ref_learner_linear.argtypes = [V, C.c_int64, C.c_int64, V, V, V, C.c_int64, V, V, V]
@@ -118,6 +120,28 @@ class Ref(_Lib):
         b = int(bs[0])
         return {"status": 0, "b": b, "s": int(bs[1]), "predicted": float(pt[0]),
                 "target": float(pt[1]), "overload": int(ov[0]),
+                "alloc": [(int(aid[i]), int(atok[i]), int(apf[i])) for i in range(b)]}
+
+    def schedule_baseline(self, policy, n_run, wait_prompt, wait_prefilled, params8, m_max, q_max,
+                          static_budget, engine_id=0):
+        import numpy as np
+        wp = np.ascontiguousarray(wait_prompt, dtype=np.int64)
+        wf = np.ascontiguousarray(wait_prefilled, dtype=np.int64)
+        pp = np.ascontiguousarray(params8, dtype=np.float64)
+        n_alloc = n_run + wp.size + 1
+        bs = np.zeros(2, dtype=np.int64)
+        pr = np.zeros(1, dtype=np.float64)
+        aid = np.zeros(n_alloc, dtype=np.int64)
+        atok = np.zeros(n_alloc, dtype=np.int64)
+        apf = np.zeros(n_alloc, dtype=np.int32)
+        rc = self.lib.ref_schedule_baseline(policy, wp.ctypes.data, wf.ctypes.data, wp.size, n_run,
+                                            pp.ctypes.data, m_max, q_max, static_budget, engine_id,
+                                            bs.ctypes.data, pr.ctypes.data, aid.ctypes.data,
+                                            atok.ctypes.data, apf.ctypes.data)
+        if rc != 0:
+            return {"status": rc}
+        b = int(bs[0])
+        return {"status": 0, "b": b, "s": int(bs[1]), "predicted": float(pr[0]),
                 "alloc": [(int(aid[i]), int(atok[i]), int(apf[i])) for i in range(b)]}
 
     def route_group(self, policy, cfg9, ttft, tpot, seed, ids, static_w, states5, qlen, has_rep,

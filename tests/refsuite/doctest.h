@@ -1,5 +1,5 @@
-// Minimal doctest-compatible harness (TEST_CASE, CHECK, CHECK_FALSE,
-// REQUIRE, CHECK_THROWS_AS, doctest::Approx) — enough to compile the
+// Minimal doctest-compatible harness (TEST_CASE, SUBCASE (one level),
+// CHECK, CHECK_FALSE, REQUIRE, CHECK_THROWS_AS, doctest::Approx) — enough to compile the
 // reference's unit-test sources unchanged against the B200 drop-in
 // (doctest itself is not vendored in the reference). Test infrastructure
 // only; written for this repo.
@@ -67,6 +67,17 @@ inline int& checks() {
   static int c = 0;
   return c;
 }
+// SUBCASE: each pass over a test case runs the subcases before the target
+// one as skipped and enters exactly the target; the runner repeats the case
+// until every subcase it met has had its pass (doctest's one-level semantics).
+struct Sub {
+  int target = 0, seen = 0;
+};
+inline Sub& sub() {
+  static Sub s;
+  return s;
+}
+inline bool enter_subcase() { return sub().seen++ == sub().target; }
 inline void fail(const char* kind, const char* expr, const char* file, int line) {
   ++failures();
   std::fprintf(stderr, "%s:%d: %s( %s ) FAILED\n", file, line, kind, expr);
@@ -81,6 +92,7 @@ inline void fail(const char* kind, const char* expr, const char* file, int line)
   static doctest::detail::Reg DOCTEST_CAT(fn, _reg)(name, __FILE__, __LINE__, fn);  \
   static void fn()
 #define TEST_CASE(name) DOCTEST_TC_(DOCTEST_CAT(doctest_case_, __COUNTER__), name)
+#define SUBCASE(name) if (doctest::detail::enter_subcase())
 
 #define CHECK(...)                                                               \
   do {                                                                           \
@@ -121,13 +133,18 @@ int main(int argc, char** argv) {
     if (only && !std::strstr(c.name, only) && !std::strstr(c.file, only)) continue;
     ++run;
     const int before = doctest::detail::failures();
-    try {
-      c.fn();
-    } catch (const doctest::detail::Abort&) {
-    } catch (const std::exception& e) {
-      ++doctest::detail::failures();
-      std::fprintf(stderr, "%s:%d: unexpected exception: %s\n", c.file, c.line, e.what());
-    }
+    auto& sub = doctest::detail::sub();
+    sub.target = 0;
+    do {
+      sub.seen = 0;
+      try {
+        c.fn();
+      } catch (const doctest::detail::Abort&) {
+      } catch (const std::exception& e) {
+        ++doctest::detail::failures();
+        std::fprintf(stderr, "%s:%d: unexpected exception: %s\n", c.file, c.line, e.what());
+      }
+    } while (++sub.target < sub.seen);
     const bool ok = doctest::detail::failures() == before;
     failed_cases += !ok;
     std::printf("[%s] %s\n", ok ? "PASS" : "FAIL", c.name);

@@ -35,6 +35,45 @@ def _unhex(v):
     return float.fromhex(v)
 
 
+# ---- schedule_baseline (engine.cpp:61-108) ------------------------------------------
+def test_baseline_batch_matches_reference_schedule_baseline():
+    cases = ops_cases.baseline_cases()
+    probs = np.zeros(len(cases), dtype=abi.BASELINE_PROBLEM)
+    rem, off = [], 0
+    for i, c in enumerate(cases):
+        r = [p - f for p, f in zip(c["prompt"], c["prefilled"])]
+        probs[i] = lens.baseline_record(c["policy"], c["n_run"], len(r), off, c["params"], c["m_max"],
+                                        c["q_max"], c["static_budget"], c["engine_id"])
+        rem += r
+        off += len(r)
+    out, tok = lens.schedule_baseline_batch(probs, np.asarray(rem, dtype=np.int32), raise_errors=False)
+    for i, want in enumerate(GOLD["baseline"]):
+        p = out[i]
+        assert int(p["status"]) == want["status"], i
+        if want["status"]:
+            continue
+        assert (int(p["b"]), int(p["s"])) == (want["b"], want["s"]), i
+        assert _close(p["predicted_ms"], _unhex(want["predicted"]), 1e-12), i
+        w0 = int(probs[i]["wait_off"])
+        alloc = [[j, 1, 0] for j in range(int(p["n_decode"]))]
+        alloc += [[1000 + k, int(tok[w0 + k]), 1] for k in range(int(p["n_prefill"]))]
+        assert alloc == want["alloc"], i
+
+
+def test_baseline_scalar_api_mirrors_reference():
+    runs = [lens.Request(id=100 + i, prompt_len=64, prefilled=64) for i in range(5)]
+    waits = [lens.Request(id=p, prompt_len=p) for p in (300, 400)]
+    plan = lens.schedule_baseline(lens.PREFILL_PRIORITY, waits, runs, ops_cases.FAST, q_max=64)
+    assert (plan.b, plan.s) == (2, 700) and all(a.is_prefill for a in plan.allocations)
+    plan = lens.schedule_baseline(lens.PREFILL_PRIORITY, [], runs, ops_cases.FAST, q_max=64)
+    assert (plan.b, plan.s) == (5, 5)
+    with pytest.raises(RuntimeError):
+        lens.schedule_baseline(lens.PREFILL_PRIORITY, [lens.Request(id=1, prompt_len=9000)], [],
+                               ops_cases.FAST)
+    with pytest.raises(ValueError):
+        lens.schedule_baseline(lens.STATIC_CHUNKED, [], runs, ops_cases.FAST, q_max=4, m_max=8192)
+
+
 # ---- K2 --------------------------------------------------------------------------
 @pytest.fixture(scope="module")
 def lens_run():

@@ -27,6 +27,7 @@ def test_golden_inputs_regenerate_identically():
     assert M.digest(ops_cases.lens_cases()) == GOLD["digest"]["lens"]
     assert M.digest(ops_cases.route_cases()) == GOLD["digest"]["route"]
     assert M.digest(ops_cases.refit_cases()) == GOLD["digest"]["refit"]
+    assert M.digest(ops_cases.baseline_cases()) == GOLD["digest"]["baseline"]
 
 
 @pytest.mark.skipif(not ref_available(), reason="compiled reference not present")
@@ -60,6 +61,18 @@ def test_reference_reproduces_route_and_refit_golden():
             assert [x.hex() for x in r["params"]] == want["params"]
 
 
+@pytest.mark.skipif(not ref_available(), reason="compiled reference not present")
+def test_reference_reproduces_baseline_golden():
+    ref = Ref()
+    for c, want in zip(ops_cases.baseline_cases(), GOLD["baseline"]):
+        r = ref.schedule_baseline(c["policy"], c["n_run"], c["prompt"], c["prefilled"], c["params"],
+                                  c["m_max"], c["q_max"], c["static_budget"], c["engine_id"])
+        assert r["status"] == want["status"]
+        if r["status"] == 0:
+            assert r["predicted"].hex() == want["predicted"] and r["s"] == want["s"]
+            assert [list(a) for a in r["alloc"]] == want["alloc"]
+
+
 def test_host_validation_precedes_device_work():
     from paper_2509_23384_b200 import abi, learner, lens
     probs = np.zeros(1, dtype=abi.LENS_PROBLEM)
@@ -70,6 +83,9 @@ def test_host_validation_precedes_device_work():
     rp["n_samples"], rp["sample_off"], rp["long_window"] = 10, 0, 64
     with pytest.raises(ValueError):
         learner.refit_batch(learner.LINEAR, rp, [1] * 3, [1] * 3, [1.0] * 3)
+    bp = lens.baseline_record(lens.STATIC_CHUNKED, 0, 4, 0, ops_cases.FAST)
+    with pytest.raises(ValueError):
+        lens.schedule_baseline_batch(bp, np.ones(2, dtype=np.int32))
 
 
 REFSUITE = ROOT / "tests" / "refsuite" / "_bin" / "refsuite"

@@ -1,7 +1,6 @@
 """The reference's own unit tests — proj/tests/test_perf_model.cpp,
 test_lens.cpp, test_router.cpp, test_learner.cpp, test_metrics.cpp,
-test_workload.cpp and test_sim.cpp (112 of its 128 cases; test_engine.cpp
-drives EngineSim step by step, which the device runs inside whole replicas),
+test_workload.cpp, test_sim.cpp and test_engine.cpp (all 128 cases),
 compiled UNMODIFIED (tests/refsuite/Makefile) against the C++ drop-in
 include/nx_servesim.hpp — run on the device path: every throughput /
 predict_latency, schedule_step, binary_search_budget, allocate_tokens,

@@ -27,3 +27,10 @@ for rate in sorted(by):
     st = max(x[1] for x in v)
     print(f"rate {rate:5.1f}: n {len(v):3d} dur ms min {ms[0]:7.1f} med {ms[len(ms)//2]:7.1f} max {ms[-1]:7.1f}  "
           f"events {ev:8.0f}  ns/event {1e6*ms[len(ms)//2]/ev:6.0f}  latest start {st:7.1f}")
+# occupancy of the launch over time: replicas in flight at 20 instants
+spans = [((x[0] - t0) / 1e6, (x[1] - t0) / 1e6) for x in tl]
+end = max(e for _, e in spans)
+print(f"sum of replica durations {sum(e - b for b, e in spans):.0f} ms over {end:.0f} ms")
+print("in flight:", " ".join(str(sum(1 for b_, e_ in spans if b_ <= end * k / 20 < e_)) for k in range(20)))
+ends = sorted(e for _, e in spans)
+print("finish quantiles ms:", " ".join(f"{ends[int(q * (len(ends) - 1))]:.0f}" for q in (0.25, 0.5, 0.75, 0.9, 0.99, 1.0)))

@@ -12,6 +12,9 @@
 //    the reference's left-fold decisions.
 #pragma once
 #include "nx_state.cuh"
+#ifdef NX_TRACE_FIT
+#include <cstdio>
+#endif
 
 namespace nxd {
 
@@ -38,8 +41,11 @@ __device__ __forceinline__ double pick5(const double v[5], int k) {
 // streamed through the instruction cache once per fit). Out of line it cost
 // 10k cycles per call: shuffles in a non-inlined function compile to
 // WARPSYNC/ENDCOLLECTIVE sequences, and the array arguments go to the stack.
+// amb[k]: some pivot the rank test looked at lies within [0.5, 2] x its
+// threshold 1e-10 * norm — a decision that rounding in the inputs could flip
+// (entries accurate to ~n u relative move a pivot by ~1e-11 norm at most).
 template <int K>
-__device__ __forceinline__ void solve5_warp_k(double (&v)[K], double (&x)[K][5], bool (&ok)[K]) {
+__device__ __forceinline__ void solve5_warp_k(double (&v)[K], double (&x)[K][5], bool (&ok)[K], bool (&amb)[K]) {
   const int lane = lane_id();
   const bool isA = lane < 25;
   const int i = isA ? lane / 5 : (lane < 30 ? lane - 25 : 0);
@@ -52,6 +58,7 @@ __device__ __forceinline__ void solve5_warp_k(double (&v)[K], double (&x)[K][5],
     for (int r = 0; r < 5; ++r)
       m = dmax(m, fabs(__shfl_sync(NX_FULL, v[k], r * 5 + (j < 5 ? j : 0))));
     ok[k] = !__any_sync(NX_FULL, isA && i == 0 && m <= 0.0);
+    amb[k] = false;
     const double scale = (isA && m > 0.0) ? 1.0 / m : 1.0;
     if (isA) v[k] *= scale;
 #pragma unroll
@@ -79,6 +86,7 @@ __device__ __forceinline__ void solve5_warp_k(double (&v)[K], double (&x)[K][5],
           piv = r;
           pv = cv[r];
         }
+      if (ok[k] && pv < 2e-10 * norm[k] && !(pv < 5e-11 * norm[k])) amb[k] = true;
       if (pv < 1e-10 * norm[k]) ok[k] = false;
       int src = lane;
       if (lane < 30) {
@@ -117,13 +125,20 @@ __device__ __forceinline__ void solve5_warp_k(double (&v)[K], double (&x)[K][5],
   }
 }
 
-__device__ __forceinline__ bool solve5_warp(double v, double x[5]) {
+template <int K>
+__device__ __forceinline__ void solve5_warp_k(double (&v)[K], double (&x)[K][5], bool (&ok)[K]) {
+  bool amb[K];
+  solve5_warp_k<K>(v, x, ok, amb);
+}
+
+__device__ __forceinline__ bool solve5_warp(double v, double x[5], bool* ambiguous = nullptr) {
   double vv[1] = {v};
   double xx[1][5];
-  bool ok[1];
-  solve5_warp_k<1>(vv, xx, ok);
+  bool ok[1], amb[1];
+  solve5_warp_k<1>(vv, xx, ok, amb);
 #pragma unroll
   for (int q = 0; q < 5; ++q) x[q] = xx[0][q];
+  if (ambiguous && amb[0]) *ambiguous = true;
   return ok[0];
 }
 
@@ -384,6 +399,9 @@ constexpr double kU = 1.1102230246251565e-16;  // 2^-53
 //   [8W+1024, 9W+1024) distinct token counts (int32)
 //   [9W+1024, 10W+1024) 1/f_S by distinct-count index (dense)
 //   [10W+1024, 10W+1024+kSTab/2) token count -> dense index (int32)
+//   then (group_base(W), nx_state.cuh) the grouped-sum arrays: sample indices
+//   by batch size and by distinct token count, their group offsets, and the
+//   per-group aggregates (8 per batch size, 4 per distinct token count)
 constexpr int kSTab = 10240;  // token-count table (bitmap fits the 1280 B stage)
 
 struct Stage {          // chronological window staged in the replica scratch
@@ -401,6 +419,13 @@ struct Stage {          // chronological window staged in the replica scratch
   double ifs_k, ifb_k;
   // fit-invariant normal-equation entries: A00 A03 A04 A33 A34 A44, t0 t3 t4
   double A00, A03, A04, A33, A34, A44, t0, t3, t4;
+  // Grouped sums (see gauged_fit_impl): samples grouped by batch size (pb, ob)
+  // and by distinct token count (ps, os); ab holds 8 aggregates per batch
+  // size for kS == ab_k, as 4 per distinct token count for kB == as_k.
+  int *pb, *ps, *ob, *os;
+  double *ab, *as, *part;
+  double ab_k, as_k, last_kB, last_kS;
+  bool grouped;
 };
 
 __device__ __forceinline__ Stage stage_of(const Ctx& c) {
@@ -418,13 +443,55 @@ __device__ __forceinline__ Stage stage_of(const Ctx& c) {
   s.us = reinterpret_cast<int*>(c.scratch + 8 * W + kFbTable);
   s.stab = c.scratch + 9 * W + kFbTable;
   s.s2id = reinterpret_cast<int*>(c.scratch + 10 * W + kFbTable);
+  const int64_t g = group_base(W), h = half_up(W);
+  s.pb = reinterpret_cast<int*>(c.scratch + g);
+  s.ps = reinterpret_cast<int*>(c.scratch + g + h);
+  s.ob = reinterpret_cast<int*>(c.scratch + g + 2 * h);
+  s.os = reinterpret_cast<int*>(c.scratch + g + 2 * h + half_up(kFbTable + 3));
+  s.ab = c.scratch + g + 2 * h + half_up(kFbTable + 3) + half_up(W + 2);
+  s.as = s.ab + 8 * kFbTable;
+  s.part = s.as + 4 * W;
   s.n = 0;
   s.tab = 0;
   s.U = 0;
   s.use_tab = false;
+  s.grouped = false;
   s.ifs_k = -1.0;
   s.ifb_k = -1.0;
+  s.ab_k = s.as_k = s.last_kB = s.last_kS = -1.0;
   return s;
+}
+
+// Stable grouping of samples [0, n) by key(i) in [0, nkeys): afterwards group
+// k is perm[off[k], off[k+1]) in ascending sample order (off: nkeys + 2 ints).
+// One warp, chunks of 32 samples in order; ranks within a chunk come from
+// __match_any_sync, so the placement is deterministic.
+template <class Key>
+__device__ void group_samples(int lane, int n, int nkeys, int* off, int* perm, Key key) {
+  __syncwarp();
+  for (int k = lane; k < nkeys + 2; k += 32) off[k] = 0;
+  __syncwarp();
+  for (int i = lane; i < n; i += 32) atomicAdd(&off[key(i) + 2], 1);
+  __syncwarp();
+  int carry = 0;  // inclusive scan: off[k + 1] = first slot of group k
+  for (int base = 0; base < nkeys + 2; base += 32) {
+    const int k = base + lane;
+    int v = k < nkeys + 2 ? off[k] : 0;
+    v = warp_incl_scan(v) + carry;
+    if (k < nkeys + 2) off[k] = v;
+    carry = __shfl_sync(NX_FULL, v, 31);
+  }
+  __syncwarp();
+  for (int base = 0; base < n; base += 32) {
+    const int i = base + lane;
+    const int k = i < n ? key(i) : -1;
+    const unsigned peers = __match_any_sync(NX_FULL, k);
+    const int rank = __popc(peers & ((1u << lane) - 1u));
+    if (i < n) perm[off[k + 1] + rank] = i;
+    __syncwarp();
+    if (i < n && rank == 0) off[k + 1] += __popc(peers);
+    __syncwarp();
+  }
 }
 
 // windowed_sse (learner.cpp:209-222), direct model evaluation, tree order
@@ -581,6 +648,32 @@ static __device__ NX_COLD void stage_window(Ctx& c, const Window& w, const Param
       rec[i].y = __longlong_as_double(static_cast<long long>(
           bits64 | (static_cast<unsigned long long>(S.s2id[si]) << 16)));
     }
+    __syncwarp();
+    // grouped sums need every batch size inside the 1/f_B table
+    S.grouped = bmax < kFbTable;
+    if (S.grouped) {
+      const double2* rc = S.rec;
+      group_samples(c.lane, w.n, S.tab + 1, S.ob, S.pb, [rc](int i) {
+        return static_cast<int>(static_cast<unsigned long long>(__double_as_longlong(rc[i].y)) & 0xffffull);
+      });
+      group_samples(c.lane, w.n, S.U, S.os, S.ps, [rc](int i) {
+        return static_cast<int>((static_cast<unsigned long long>(__double_as_longlong(rc[i].y)) >> 16) & 0xffffull);
+      });
+#ifdef NX_TRACE_FIT
+      __syncwarp();
+      if (c.lane == 0 && w.n == 1024) {
+        int bad = 0, badk = 0;
+        for (int g = 0; g <= S.tab; ++g)
+          for (int j = S.ob[g]; j < S.ob[g + 1]; ++j)
+            if ((static_cast<unsigned long long>(__double_as_longlong(rc[S.pb[j]].y)) & 0xffffull) != (unsigned)g) ++bad;
+        for (int k = 0; k < S.U; ++k)
+          for (int j = S.os[k]; j < S.os[k + 1]; ++j)
+            if (((static_cast<unsigned long long>(__double_as_longlong(rc[S.ps[j]].y)) >> 16) & 0xffffull) != (unsigned)k) ++badk;
+        printf("GROUPCHECK n %d tab %d U %d ob_end %d os_end %d bad_b %d bad_s %d\n", w.n, S.tab, S.U, S.ob[S.tab + 1], S.os[S.U], bad, badk);
+      }
+      __syncwarp();
+#endif
+    }
   }
   __syncwarp();
 }
@@ -646,6 +739,128 @@ static __device__ __forceinline__ void pass_range(const double2* rec, const doub
 __device__ __forceinline__ void team_sync() {
   asm volatile("bar.sync 1, %0;" ::"r"(32 * kRefitWarps) : "memory");
 }
+
+// ---- grouped sums ------------------------------------------------------------
+// Every (kB,kS)-dependent entry is a sum of positive per-sample terms
+// g(1/f_B(b)) * h(1/f_S(s)) * m(b, s, 1/y). While kS stays fixed (a move of kB
+// alone) each entry is a sum over batch sizes b of 1/f_B(b) (or its square)
+// times one of 8 per-b aggregates that depend on kS only (ab); while kB stays
+// fixed, a sum over the distinct token counts of 1/f_S (or its square) times
+// one of 4 per-count aggregates that depend on kB only (as). The coordinate
+// search moves one coordinate at a time and mostly misses, so ~85% of its
+// fits become sums over <= 1024 batch sizes / the distinct token counts
+// instead of passes over the window; the aggregates are rebuilt only after a
+// move is accepted. Terms stay positive, so the closed-form SSE bound holds.
+
+// Aggregate rebuilds. The grouped sample order is cut into one contiguous
+// chunk per team lane (balanced however skewed the groups are: a low-load
+// replica has few batch sizes, each with hundreds of samples). A lane writes
+// the groups that lie inside its chunk; a group cut by a chunk boundary
+// leaves per-lane partials (tail: the group it ends its chunk in, head: the
+// group it starts its chunk in) that a second phase adds in lane order.
+// Deterministic for a given team size.
+//   ab[8b + .] (kS of the stab table), over the samples with batch size b:
+//     F w, s F w, F^2 w, s F^2 w, s^2 F^2 w, s^2 F w, F v, s F v
+//   as[4k + .] (kB of the ifb table), over the samples with token count us[k]:
+//     G w, G^2 w, b G w, G v
+//   (F = 1/f_S(s), G = 1/f_B(b), v = 1/y, w = v^2)
+template <int NV>
+__device__ __forceinline__ void agg_terms(const TeamTask& t, const double2 r, double (&a)[8]) {
+  const unsigned long long v = static_cast<unsigned long long>(__double_as_longlong(r.y));
+  if (NV == 8) {
+    const double sv = static_cast<double>(static_cast<int>(v >> 32));
+    const double F = t.stab[(v >> 16) & 0xffffull];
+    const double Fy = F * r.x, Fw = Fy * r.x, F2w = F * Fw;
+    a[0] += Fw; a[1] += sv * Fw; a[2] += F2w; a[3] += sv * F2w;
+    a[4] += sv * (sv * F2w); a[5] += sv * (sv * Fw); a[6] += Fy; a[7] += sv * Fy;
+  } else {
+    const int bi = static_cast<int>(v & 0xffffull);
+    const double G = t.ifb[bi];
+    const double Gy = G * r.x, Gw = Gy * r.x;
+    a[0] += Gw; a[1] += G * Gw; a[2] += static_cast<double>(bi) * Gw; a[3] += Gy;
+  }
+}
+template <int NV>
+__device__ __forceinline__ int agg_key(const double2 r) {
+  const unsigned long long v = static_cast<unsigned long long>(__double_as_longlong(r.y));
+  return NV == 8 ? static_cast<int>(v & 0xffffull) : static_cast<int>((v >> 16) & 0xffffull);
+}
+template <int NV>
+static __device__ void rebuild_groups(const TeamTask& t, int gl, int nl, int team) {
+  const int* perm = NV == 8 ? t.pb : t.ps;
+  const int* off = NV == 8 ? t.ob : t.os;
+  const int ng = NV == 8 ? t.tab + 1 : t.U;
+  double* out = NV == 8 ? t.ab : t.as;
+  double* head = t.part;            // [nl][8]
+  double* tail = t.part + 8 * nl;   // [nl][8]
+  const int per = (t.n + nl - 1) / nl;
+  const int lo = min(t.n, gl * per), hi = min(t.n, lo + per);
+  if (lo < hi) {
+    double a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    int g = agg_key<NV>(t.rec[perm[lo]]);
+    auto flush = [&](int gg) {
+      const int g0 = off[gg], g1 = off[gg + 1];
+      double* o = g0 >= lo && g1 <= hi ? out + NV * gg : (g0 < lo ? head : tail) + 8 * gl;
+#pragma unroll
+      for (int q = 0; q < NV; ++q) o[q] = a[q];
+    };
+    for (int j = lo; j < hi; ++j) {
+      const double2 r = t.rec[perm[j]];
+      const int k = agg_key<NV>(r);
+      if (k != g) {
+        flush(g);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) a[q] = 0.0;
+        g = k;
+      }
+      agg_terms<NV>(t, r, a);
+    }
+    flush(g);
+  }
+  if (team > 1) team_sync();
+  else __syncwarp();
+  // empty groups, and groups cut by chunk boundaries: tail of the first lane
+  // + heads of the rest
+  for (int gg = gl; gg < ng; gg += nl) {
+    const int g0 = off[gg], g1 = off[gg + 1];
+    if (g0 >= g1) {  // no samples: the sums over groups read every slot
+#pragma unroll
+      for (int q = 0; q < NV; ++q) out[NV * gg + q] = 0.0;
+      continue;
+    }
+    const int l0 = g0 / per, l1 = (g1 - 1) / per;
+    if (l0 == l1) continue;
+    double a[8];
+#pragma unroll
+    for (int q = 0; q < NV; ++q) a[q] = tail[8 * l0 + q];  // the group starts in l0's chunk
+    for (int l = l0 + 1; l <= l1; ++l)
+#pragma unroll
+      for (int q = 0; q < NV; ++q) a[q] += head[8 * l + q];
+#pragma unroll
+    for (int q = 0; q < NV; ++q) out[NV * gg + q] = a[q];
+  }
+}
+// The 11 entries (pass_range order) from ab and the ifb table (kB move).
+static __device__ void sum_over_b(const TeamTask& t, int g0, int gstep, double a[11]) {
+  for (int b = 1 + g0; b <= t.tab; b += gstep) {
+    const double g = t.ifb[b], bb = static_cast<double>(b);
+    const double* P = t.ab + 8 * b;
+    const double gP0 = g * P[0], gP1 = g * P[1], g2 = g * g;
+    a[0] += gP0; a[1] += gP1; a[2] += g2 * P[2]; a[3] += g2 * P[3]; a[4] += g2 * P[4];
+    a[5] += bb * gP0; a[6] += gP1; a[7] += bb * gP1; a[8] += g * P[5]; a[9] += g * P[6]; a[10] += g * P[7];
+  }
+}
+// The 11 entries from as and the stab table (kS move).
+static __device__ void sum_over_s(const TeamTask& t, int g0, int gstep, double a[11]) {
+  for (int k = g0; k < t.U; k += gstep) {
+    const double h = t.stab[k], sv = static_cast<double>(t.us[k]);
+    const double* Q = t.as + 4 * k;
+    const double hQ0 = h * Q[0], h2Q1 = h * (h * Q[1]), hQ2 = h * Q[2], hQ3 = h * Q[3];
+    a[0] += hQ0; a[1] += sv * hQ0; a[2] += h2Q1; a[3] += sv * h2Q1; a[4] += sv * (sv * h2Q1);
+    a[5] += hQ2; a[6] += sv * hQ0; a[7] += sv * hQ2; a[8] += sv * (sv * hQ0); a[9] += hQ3; a[10] += sv * hQ3;
+  }
+}
+
 // Contiguous, 256-aligned share of [0, n) for team member k of `team`.
 __device__ __forceinline__ void team_range(int n, int k, int team, int& lo, int& hi) {
   const int per = ((n + 255) / 256 + team - 1) / team * 256;
@@ -653,25 +868,64 @@ __device__ __forceinline__ void team_range(int n, int k, int team, int& lo, int&
   hi = min(n, lo + per);
 }
 
-// Helper warps of the refit team: run their share of each fit pass the
-// leader (warp 1) publishes, until it publishes op -1.
+// Member k's share of task t; ops 1-3 return this warp's totals in out[11]
+// (warp_sum), ops 4-5 write aggregates.
+__device__ __forceinline__ void team_work(const TeamTask& t, int k, int team, int lane, double out[11]) {
+  if (t.op == 1) {
+    int lo, hi;
+    team_range(t.n, k, team, lo, hi);
+    pass_range(t.rec, t.stab, t.ifb, t.tab, t.kB, lo, hi, lane, out);
+  } else if (t.op == 4) {
+    rebuild_groups<8>(t, 32 * k + lane, 32 * team, team);
+  } else if (t.op == 5) {
+    rebuild_groups<4>(t, 32 * k + lane, 32 * team, team);
+  } else {
+    double a[11] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    if (t.op == 2) sum_over_b(t, 32 * k + lane, 32 * team, a);
+    else sum_over_s(t, 32 * k + lane, 32 * team, a);
+#pragma unroll
+    for (int q = 0; q < 11; ++q) out[q] = warp_sum(a[q]);
+  }
+}
+
+// Helper warps of the refit team: run their share of each task the leader
+// (warp 1) publishes, until it publishes op -1.
 static __device__ NX_COLD void team_helper(Ctx& c) {
   const int k = c.worker - 1;
   while (true) {
     team_sync();  // task published
     const TeamTask t = c.rs->team;
     if (t.op < 0) break;
-    int lo, hi;
-    team_range(t.n, k, kRefitWarps, lo, hi);
     double part[11];
-    pass_range(t.rec, t.stab, t.ifb, t.tab, t.kB, lo, hi, c.lane, part);
-    if (c.lane == 0)
+    team_work(t, k, kRefitWarps, c.lane, part);
+    if (c.lane == 0 && t.op <= 3)
       for (int q = 0; q < 11; ++q) c.rs->team_part[k][q] = part[q];
-    team_sync();  // partial totals written
+    team_sync();  // partial totals / aggregates written
   }
 }
 
+// Leader side: run t over the team (or alone) and combine the members'
+// totals in member order.
+static __device__ void run_task(Ctx& c, const TeamTask& t, double tot[11]) {
+  if (c.team > 1) {
+    if (c.lane == 0) c.rs->team = t;
+    team_sync();  // publish
+    team_work(t, 0, c.team, c.lane, tot);
+    team_sync();  // members done
+    if (t.op <= 3)
+      for (int k = 1; k < c.team; ++k)
+#pragma unroll
+        for (int q = 0; q < 11; ++q) tot[q] += c.rs->team_part[k][q];
+  } else {
+    team_work(t, 0, 1, c.lane, tot);
+  }
+  __syncwarp();
+}
+
 static __device__ FitOut gauged_fit_impl(Ctx& c, Stage& S, const Params& cur, double kB, double kS);
+static __device__ FitOut finish_fit(Ctx& c, const Stage& S, const Params& cur, double kB, double kS, double e,
+                                   bool* ambiguous);
+static __device__ FitOut exact_fit(Ctx& c, const Stage& S, const Params& cur, double kB, double kS);
 static __device__ FitOut gauged_fit(Ctx& c, Stage& S, const Params& cur, double kB, double kS) {
   const long long t0 = nx_clock();
   FitOut o = gauged_fit_impl(c, S, cur, kB, kS);
@@ -682,7 +936,24 @@ static __device__ NX_COLD FitOut gauged_fit_impl(Ctx& c, Stage& S, const Params&
   if (c.lane == 0) count(c.rs->work[5], 1);
   const int n = S.n;
   const long long tf0 = nx_clock();
-  if (kB != S.ifb_k) {
+  // Which sum: over b (kS unchanged since ab was built), over the distinct
+  // token counts (kB unchanged since as was built), either after rebuilding
+  // its aggregates when the previous fit shared the other coordinate, or a
+  // pass over the samples. 1/f >= 1e100 never occurs under the guard, so the
+  // reference's max(fB fS, 1e-300) floor (= a 1e300 cap on the product of
+  // the inverses) cannot bind there.
+  int op = 1;
+  bool rebuild = false;
+  if (S.grouped && kB >= 1e-100 && kS >= 1e-100) {
+    if (kS == S.ab_k) op = 2;
+    else if (kB == S.as_k) op = 3;
+    else if (kB == S.last_kB) op = 3, rebuild = true;
+    else if (kS == S.last_kS) op = 2, rebuild = true;
+  }
+  S.last_kB = kB;
+  S.last_kS = kS;
+  const bool need_fb = op != 3 || rebuild, need_fs = op != 2 || rebuild;
+  if (need_fb && kB != S.ifb_k) {
     __syncwarp();
 #pragma unroll 4
     for (int b = 1 + c.lane; b <= S.tab; b += 32)
@@ -691,7 +962,7 @@ static __device__ NX_COLD FitOut gauged_fit_impl(Ctx& c, Stage& S, const Params&
     __syncwarp();
   }
   const bool new_s = kS != S.ifs_k;
-  if (new_s && S.use_tab) {
+  if (need_fs && new_s && S.use_tab) {
     __syncwarp();
 #pragma unroll 4
     for (int k = c.lane; k < S.U; k += 32)
@@ -700,29 +971,68 @@ static __device__ NX_COLD FitOut gauged_fit_impl(Ctx& c, Stage& S, const Params&
   }
   const long long tf1 = nx_clock();
   if (c.lane == 0) count(c.rs->cycles[7], tf1 - tf0);
-  // per-entry totals of the pass (fixed combination order across the team;
-  // every term is positive, so the closed-form SSE bound covers any order)
+  // per-entry totals (fixed combination order across the team; every term is
+  // positive, so the closed-form SSE bound covers any order)
   double tot[11];
-  if (S.use_tab && c.team > 1) {
-    if (c.lane == 0) {
-      c.rs->team.rec = S.rec;
-      c.rs->team.stab = S.stab;
-      c.rs->team.ifb = S.ifb;
-      c.rs->team.kB = kB;
-      c.rs->team.n = n;
-      c.rs->team.tab = S.tab;
-      c.rs->team.op = 1;
+  if (S.use_tab) {
+    TeamTask t;
+    t.rec = S.rec;
+    t.stab = S.stab;
+    t.ifb = S.ifb;
+    t.pb = S.pb;
+    t.ps = S.ps;
+    t.ob = S.ob;
+    t.os = S.os;
+    t.us = S.us;
+    t.ab = S.ab;
+    t.as = S.as;
+    t.part = S.part;
+    t.kB = kB;
+    t.n = n;
+    t.tab = S.tab;
+    t.U = S.U;
+    if (rebuild) {
+      t.op = op == 2 ? 4 : 5;
+      run_task(c, t, tot);
+      if (op == 2) S.ab_k = kS;
+      else S.as_k = kB;
+#ifdef NX_TRACE_FIT
+      if (op == 2 && n == 1024 && c.lane == 0) {
+        const int per = (n + 95) / 96;
+        for (int g = 1; g <= S.tab; ++g) {
+          double d[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+          for (int j = S.ob[g]; j < S.ob[g + 1]; ++j) agg_terms<8>(t, S.rec[S.pb[j]], d);
+          for (int q = 0; q < 8; ++q)
+            if (fabs(d[q] - S.ab[8 * g + q]) > 1e-9 * fabs(d[q])) {
+              printf("    AB g %d q %d direct %.17g ab %.17g span [%d,%d) lanes %d..%d\n", g, q, d[q], S.ab[8 * g + q],
+                     S.ob[g], S.ob[g + 1], S.ob[g] / per, (S.ob[g + 1] - 1) / per);
+              break;
+            }
+        }
+      }
+#endif
     }
-    team_sync();  // publish
-    int lo, hi;
-    team_range(n, 0, c.team, lo, hi);
-    pass_range(S.rec, S.stab, S.ifb, S.tab, kB, lo, hi, c.lane, tot);
-    team_sync();  // helpers' totals written
-    for (int k = 1; k < c.team; ++k)
-#pragma unroll
-      for (int q = 0; q < 11; ++q) tot[q] += c.rs->team_part[k][q];
-  } else if (S.use_tab) {
-    pass_range(S.rec, S.stab, S.ifb, S.tab, kB, 0, n, c.lane, tot);
+    t.op = op;
+    run_task(c, t, tot);
+#ifdef NX_TRACE_FIT
+    if (op != 1 && S.n == 1024) {
+      if (kS != S.ifs_k) {
+        for (int k = c.lane; k < S.U; k += 32) S.stab[k] = 1.0 / raw_factor(kS, static_cast<double>(S.us[k]));
+        S.ifs_k = kS;
+      }
+      if (kB != S.ifb_k) {
+        for (int b = 1 + c.lane; b <= S.tab; b += 32) S.ifb[b] = 1.0 / raw_factor(kB, static_cast<double>(b));
+        S.ifb_k = kB;
+      }
+      __syncwarp();
+      double chk[11];
+      t.op = 1;
+      run_task(c, t, chk);
+      for (int q = 0; q < 11; ++q)
+        if (c.lane == 0 && fabs(chk[q] - tot[q]) > 1e-9 * fabs(chk[q]))
+          printf("    op %d kB %.6g kS %.6g entry %d grouped %.17g pass %.17g\n", op, kB, kS, q, tot[q], chk[q]);
+    }
+#endif
   } else {
     double a01 = 0, a02 = 0, a11 = 0, a12 = 0, a22 = 0, a13 = 0, a14 = 0, a23 = 0, a24 = 0;
     double t1 = 0, t2 = 0;
@@ -750,13 +1060,58 @@ static __device__ NX_COLD FitOut gauged_fit_impl(Ctx& c, Stage& S, const Params&
     tot[4] = warp_sum(a22); tot[5] = warp_sum(a13); tot[6] = warp_sum(a14); tot[7] = warp_sum(a23);
     tot[8] = warp_sum(a24); tot[9] = warp_sum(t1); tot[10] = warp_sum(t2);
   }
-  S.ifs_k = kS;
+  if (need_fs) S.ifs_k = kS;
   if (c.lane == 0) count(c.rs->cycles[9], nx_clock() - tf1);
   const long long tf2 = nx_clock();
   const double u15[15] = {S.A00, tot[0], tot[1], S.A03, S.A04, tot[2], tot[3], tot[5], tot[6],
                           tot[4], tot[7], tot[8], S.A33, S.A34, S.A44};
   const double t5[5] = {S.t0, tot[9], tot[10], S.t3, S.t4};
-  const double e = normal_elem(u15, t5);
+  bool ambiguous = false;
+  FitOut out = finish_fit(c, S, cur, kB, kS, normal_elem(u15, t5), &ambiguous);
+  // a rank test too close to call on the fast sums: the reference's exact ones decide
+  if (ambiguous) out = exact_fit(c, S, cur, kB, kS);
+  if (c.lane == 0) count(c.rs->cycles[13], nx_clock() - tf2);
+  return out;
+}
+
+// The reference's exact normal equations for (kB, kS): rows (1, 1/f, s/f, b,
+// s) / y with f = max(fB fS, 1e-300), accumulated left to right in window
+// order (Ols5::add, learner.cpp:62-75, 228-245) — one fold lane per entry.
+// The coordinate search ranks candidates on the fast sums (every ranking
+// certified); the winner's coefficients are recomputed here so the learner
+// adopts the reference's values, not values a few ulps of the window sums
+// away (the 5x5 solve amplifies those by the system's condition number).
+static __device__ NX_COLD FitOut exact_fit(Ctx& c, const Stage& S, const Params& cur, double kB, double kS) {
+  const int n = S.n;
+  double acc = 0.0;
+  for (int base = 0; base < n; base += 32) {
+    const int i = base + c.lane;
+    __syncwarp();
+    if (i < n) {
+      const double b = S.sb[i], sv = S.ss[i];
+      double f = raw_factor(kB, b) * raw_factor(kS, sv);
+      f = (f < 1e-300) ? 1e-300 : f;
+      const double iy = 1.0 / S.sy[i];
+      double* row = c.chunk + c.lane * 5;
+      row[0] = 1.0 * iy;
+      row[1] = (1.0 / f) * iy;
+      row[2] = (sv / f) * iy;
+      row[3] = b * iy;
+      row[4] = sv * iy;
+    }
+    __syncwarp();
+    fold_chunk(c, min(32, n - base), acc);
+  }
+  const int src = c.lane < 25 ? slot_of(c.lane / 5, c.lane % 5) : (c.lane < 30 ? 15 + c.lane - 25 : 0);
+  const double e = __shfl_sync(NX_FULL, acc, src);
+  return finish_fit(c, S, cur, kB, kS, e, nullptr);
+}
+
+// Solve, ridge and trust region of gauged_fit (learner.cpp:246-297) from the
+// normal equations e (lane element: A^T A slot or A^T b).
+static __device__ NX_COLD FitOut finish_fit(Ctx& c, const Stage& S, const Params& cur, double kB, double kS,
+                                            double e, bool* ambiguous) {
+  const int n = S.n;
   const double y2 = static_cast<double>(n);  // sum of 1.0 * 1.0 (learner.cpp:73)
   const double prior[5] = {cur.tau0, cur.w0 / cur.p_max, cur.ws / cur.p_max, cur.tauB, cur.tauS};
   FitOut out;
@@ -767,10 +1122,11 @@ static __device__ NX_COLD FitOut gauged_fit_impl(Ctx& c, Stage& S, const Params&
   double x[5];
   double vk[2] = {e, ridge_elem(e, 1e-7, prior)};
   double xk[2][5];
-  bool okk[2];
+  bool okk[2], amb[2];
   const long long ts5 = nx_clock();
-  solve5_warp_k<2>(vk, xk, okk);
+  solve5_warp_k<2>(vk, xk, okk, amb);
   if (c.lane == 0) count(c.rs->cycles[15], nx_clock() - ts5);
+  if (ambiguous && amb[0]) *ambiguous = true;
   if (!okk[0]) return out;
 #pragma unroll
   for (int q = 0; q < 5; ++q) x[q] = xk[0][q];
@@ -807,10 +1163,11 @@ static __device__ NX_COLD FitOut gauged_fit_impl(Ctx& c, Stage& S, const Params&
     lambda = (v < 1e-7) ? v : 1e-7;
   }
   if (lambda == 1e-7) {
+    if (ambiguous && amb[1]) *ambiguous = true;
     if (!okk[1]) return out;
 #pragma unroll
     for (int q = 0; q < 5; ++q) x[q] = xk[1][q];
-  } else if (lambda > 1e-14 && !solve5_warp(ridge_elem(e, lambda, prior), x)) {
+  } else if (lambda > 1e-14 && !solve5_warp(ridge_elem(e, lambda, prior), x, ambiguous)) {
     return out;
   }
   const double tau0 = x[0] < 0.0 ? 0.0 : x[0];
@@ -834,7 +1191,6 @@ static __device__ NX_COLD FitOut gauged_fit_impl(Ctx& c, Stage& S, const Params&
   out.p = p;
   const double xp[5] = {p.tau0, aa, cc, p.tauB, p.tauS};  // T(p) == xp . row
   closed_sse(e, xp, n, y2, out.err, out.bound);
-  if (c.lane == 0) count(c.rs->cycles[13], nx_clock() - tf2);
   return out;
 }
 
@@ -887,6 +1243,10 @@ static __device__ NX_COLD void update_structural(Ctx& c, int e) {
   double th0 = log(cur.kB), th1 = log(cur.kS);
   double st0 = 0.5, st1 = 0.5;
   FitOut best = gauged_fit(c, S, cur, exp(th0), exp(th1));
+#ifdef NX_TRACE_FIT
+  const bool tr = g.seen == 1024;
+  if (tr && c.lane == 0) printf("REFIT e=%d n=%d init err %.17g base %.17g\n", e, n, best.err, base.err);
+#endif
   if (!isfinite(best.err)) {
     __syncwarp();
     if (c.lane == 0) g.cnt[5] += 1;
@@ -897,6 +1257,10 @@ static __device__ NX_COLD void update_structural(Ctx& c, int e) {
   for (int a = 0; a < 3; ++a) {
     for (int bq = 0; bq < 3; ++bq) {
       const FitOut cand = gauged_fit(c, S, cur, kbs[a], kss[bq]);
+#ifdef NX_TRACE_FIT
+      if (tr && c.lane == 0)
+        printf("  grid kB %.17g kS %.17g err %.17g bound %.3g best %.17g\n", kbs[a], kss[bq], cand.err, cand.bound, best.err);
+#endif
       if (isfinite(cand.err) && less_scaled(c, S, cand, best, shrink)) {
         th0 = log(kbs[a]);
         th1 = log(kss[bq]);
@@ -916,6 +1280,11 @@ static __device__ NX_COLD void update_structural(Ctx& c, int e) {
         tc = (v < lo) ? lo : ((hi < v) ? hi : v);
         if (tc == (cdim == 0 ? th0 : th1)) continue;
         const FitOut cand = gauged_fit(c, S, cur, exp(t0), exp(t1));
+#ifdef NX_TRACE_FIT
+        if (tr && c.lane == 0)
+          printf("  sweep %d c %d kB %.17g kS %.17g err %.17g bound %.3g best %.17g\n", sweep, cdim, exp(t0), exp(t1),
+                 cand.err, cand.bound, best.err);
+#endif
         if (isfinite(cand.err) && less_scaled(c, S, cand, best, shrink)) {
           th0 = t0;
           th1 = t1;
@@ -929,6 +1298,12 @@ static __device__ NX_COLD void update_structural(Ctx& c, int e) {
     }
     const double smax = (st0 < st1) ? st1 : st0;
     if (!improved && smax < 1e-5) break;
+  }
+  // the winner's coefficients from the reference's exact normal equations
+  {
+    const FitOut ex = exact_fit(c, S, cur, best.p.kB, best.p.kS);
+    if (isfinite(ex.err)) best = ex;
+    else best.err = ex.err;  // the exact system is singular: the reference fails this fit too
   }
   // reject if invalid or worse than the current model (learner.cpp:432-435)
   bool worse;

@@ -33,19 +33,34 @@ constexpr int kSimWarps = 1 + kRefitWarps;   // + the event-loop warp
 constexpr int kMaxSmIds = 1024;              // %smid bound of the kernel's SM bookkeeping
 constexpr int kSchedCtlInts = 3 + 2 * kMaxSmIds;
 
-// One fit pass split across the refit team (nx_learner.cuh::team_pass).
+// One piece of fit work split across the refit team (nx_learner.cuh::team_work).
 struct TeamTask {
   const double2* rec;
   const double* stab;
   const double* ifb;
+  const int* pb;    // grouped sums: sample order by batch size / by distinct s
+  const int* ps;
+  const int* ob;
+  const int* os;
+  const int* us;
+  double* ab;       // per-b / per-distinct-s aggregates
+  double* as;
+  double* part;     // rebuild partials of groups cut by chunk boundaries
   double kB;
-  int n, tab, op;  // op: 1 run a pass, -1 leave
+  int n, tab, U;
+  int op;           // 1 sample pass, 2 sum over b, 3 sum over s, 4 / 5 rebuild ab / as, -1 leave
 };
 
+// Scratch offsets (doubles) of the structural tier's grouped sums, after the
+// s -> index table (nx_learner.cuh layout).
+__host__ __device__ __forceinline__ int64_t group_base(int64_t W) { return 10 * W + kFbTable + 5120; }
+__host__ __device__ __forceinline__ int64_t half_up(int64_t v) { return (v + 1) / 2; }
 // Doubles of one warp's learner scratch for long_window W (nx_learner.cuh
 // layout; host: capi.cpp fill_descriptors allocates two per replica).
 __host__ __device__ __forceinline__ int64_t refit_scratch_stride(int64_t W) {
-  return (10 * W + kFbTable + 5120 + 64 + 31) / 32 * 32;
+  const int64_t groups =
+      2 * half_up(W) + half_up(kFbTable + 3) + half_up(W + 2) + 8 * kFbTable + 4 * W + 2 * 8 * 32 * kRefitWarps;
+  return (group_base(W) + groups + 64 + 31) / 32 * 32;
 }
 
 // Engine scalars (EngineSim + OnlineLearner + TradeoffEstimator + router view)

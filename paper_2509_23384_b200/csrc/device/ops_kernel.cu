@@ -387,7 +387,7 @@ __global__ void __launch_bounds__(32) nx_refit_kernel(int kind, const nx_refit_p
 
 // Scratch doubles one refit warp needs for long_window W (nx_learner.cuh layout).
 extern "C" int64_t nx_refit_scratch_per(int64_t W) {
-  return (10 * W + nxd::kFbTable + 5120 + 64 + 31) / 32 * 32;
+  return nxd::refit_scratch_stride(W);
 }
 
 extern "C" cudaError_t nx_launch_lens(const nx_lens_problem* probs, int n, const int32_t* rem,

@@ -303,7 +303,7 @@ void fill_descriptors(nx_sim& h) {
     sess_off += ns;
     // learner scratch for the event-loop warp and the refit leader
     // (nx_state.cuh refit_scratch_stride)
-    scratch_off += 2 * ((10 * static_cast<int64_t>(c.long_window) + 1024 + 5120 + 64 + 31) / 32 * 32);
+    scratch_off += 2 * nx_refit_scratch_per(static_cast<int64_t>(c.long_window));
     for (const auto& ec : c.engines) {
       NxEngineDesc e;
       std::memset(&e, 0, sizeof e);

@@ -465,20 +465,22 @@ __device__ __forceinline__ Stage stage_of(const Ctx& c) {
 // Stable grouping of samples [0, n) by key(i) in [0, nkeys): afterwards group
 // k is perm[off[k], off[k+1]) in ascending sample order (off: nkeys + 2 ints).
 // One warp, chunks of 32 samples in order; ranks within a chunk come from
-// __match_any_sync, so the placement is deterministic.
+// __match_any_sync, so the placement is deterministic. The counters live in
+// `work` (shared memory, >= nkeys + 2 ints) when given, else in `off`.
 template <class Key>
-__device__ void group_samples(int lane, int n, int nkeys, int* off, int* perm, Key key) {
+__device__ void group_samples(int lane, int n, int nkeys, int* off, int* perm, Key key, int* work) {
+  int* cnt = work ? work : off;
   __syncwarp();
-  for (int k = lane; k < nkeys + 2; k += 32) off[k] = 0;
+  for (int k = lane; k < nkeys + 2; k += 32) cnt[k] = 0;
   __syncwarp();
-  for (int i = lane; i < n; i += 32) atomicAdd(&off[key(i) + 2], 1);
+  for (int i = lane; i < n; i += 32) atomicAdd(&cnt[key(i) + 2], 1);
   __syncwarp();
-  int carry = 0;  // inclusive scan: off[k + 1] = first slot of group k
+  int carry = 0;  // inclusive scan: cnt[k + 1] = first slot of group k
   for (int base = 0; base < nkeys + 2; base += 32) {
     const int k = base + lane;
-    int v = k < nkeys + 2 ? off[k] : 0;
+    int v = k < nkeys + 2 ? cnt[k] : 0;
     v = warp_incl_scan(v) + carry;
-    if (k < nkeys + 2) off[k] = v;
+    if (k < nkeys + 2) cnt[k] = v;
     carry = __shfl_sync(NX_FULL, v, 31);
   }
   __syncwarp();
@@ -487,11 +489,14 @@ __device__ void group_samples(int lane, int n, int nkeys, int* off, int* perm, K
     const int k = i < n ? key(i) : -1;
     const unsigned peers = __match_any_sync(NX_FULL, k);
     const int rank = __popc(peers & ((1u << lane) - 1u));
-    if (i < n) perm[off[k + 1] + rank] = i;
+    if (i < n) perm[cnt[k + 1] + rank] = i;
     __syncwarp();
-    if (i < n && rank == 0) off[k + 1] += __popc(peers);
+    if (i < n && rank == 0) cnt[k + 1] += __popc(peers);
     __syncwarp();
   }
+  if (work)
+    for (int k = lane; k < nkeys + 2; k += 32) off[k] = cnt[k];
+  __syncwarp();
 }
 
 // windowed_sse (learner.cpp:209-222), direct model evaluation, tree order
@@ -653,12 +658,14 @@ static __device__ NX_COLD void stage_window(Ctx& c, const Window& w, const Param
     S.grouped = bmax < kFbTable;
     if (S.grouped) {
       const double2* rc = S.rec;
+      // counters in the (not yet built) shared 1/f_S table when it is there
+      int* work = c.fsm && S.U + 2 <= 2 * c.fsm_cap ? reinterpret_cast<int*>(c.fsm + kFbTable) : nullptr;
       group_samples(c.lane, w.n, S.tab + 1, S.ob, S.pb, [rc](int i) {
         return static_cast<int>(static_cast<unsigned long long>(__double_as_longlong(rc[i].y)) & 0xffffull);
-      });
+      }, work);
       group_samples(c.lane, w.n, S.U, S.os, S.ps, [rc](int i) {
         return static_cast<int>((static_cast<unsigned long long>(__double_as_longlong(rc[i].y)) >> 16) & 0xffffull);
-      });
+      }, work);
 #ifdef NX_TRACE_FIT
       __syncwarp();
       if (c.lane == 0 && w.n == 1024) {
@@ -925,7 +932,7 @@ static __device__ void run_task(Ctx& c, const TeamTask& t, double tot[11]) {
 static __device__ FitOut gauged_fit_impl(Ctx& c, Stage& S, const Params& cur, double kB, double kS);
 static __device__ FitOut finish_fit(Ctx& c, const Stage& S, const Params& cur, double kB, double kS, double e,
                                    bool* ambiguous);
-static __device__ FitOut exact_fit(Ctx& c, const Stage& S, const Params& cur, double kB, double kS);
+static __device__ FitOut exact_fit(Ctx& c, Stage& S, const Params& cur, double kB, double kS);
 static __device__ FitOut gauged_fit(Ctx& c, Stage& S, const Params& cur, double kB, double kS) {
   const long long t0 = nx_clock();
   FitOut o = gauged_fit_impl(c, S, cur, kB, kS);
@@ -1013,7 +1020,9 @@ static __device__ NX_COLD FitOut gauged_fit_impl(Ctx& c, Stage& S, const Params&
 #endif
     }
     t.op = op;
+    const long long tq = nx_clock();
     run_task(c, t, tot);
+    if (c.lane == 0 && op != 1) count(c.rs->cycles[11], nx_clock() - tq);
 #ifdef NX_TRACE_FIT
     if (op != 1 && S.n == 1024) {
       if (kS != S.ifs_k) {
@@ -1081,17 +1090,34 @@ static __device__ NX_COLD FitOut gauged_fit_impl(Ctx& c, Stage& S, const Params&
 // certified); the winner's coefficients are recomputed here so the learner
 // adopts the reference's values, not values a few ulps of the window sums
 // away (the 5x5 solve amplifies those by the system's condition number).
-static __device__ NX_COLD FitOut exact_fit(Ctx& c, const Stage& S, const Params& cur, double kB, double kS) {
+static __device__ NX_COLD FitOut exact_fit(Ctx& c, Stage& S, const Params& cur, double kB, double kS) {
   const int n = S.n;
+  // f_B by batch size and f_S by distinct token count (the reference's
+  // per-sample expm1 values) in the fit tables' storage, which the next fit
+  // then rebuilds
+  const bool tab = S.use_tab && S.grouped;
+  if (tab) {
+    __syncwarp();
+    for (int b = 1 + c.lane; b <= S.tab; b += 32) S.ifb[b] = raw_factor(kB, static_cast<double>(b));
+    for (int k = c.lane; k < S.U; k += 32) S.stab[k] = raw_factor(kS, static_cast<double>(S.us[k]));
+    S.ifb_k = S.ifs_k = -1.0;
+    __syncwarp();
+  }
   double acc = 0.0;
   for (int base = 0; base < n; base += 32) {
     const int i = base + c.lane;
     __syncwarp();
     if (i < n) {
       const double b = S.sb[i], sv = S.ss[i];
-      double f = raw_factor(kB, b) * raw_factor(kS, sv);
+      double f;
+      if (tab) {
+        const unsigned long long v = static_cast<unsigned long long>(__double_as_longlong(S.rec[i].y));
+        f = S.ifb[v & 0xffffull] * S.stab[(v >> 16) & 0xffffull];
+      } else {
+        f = raw_factor(kB, b) * raw_factor(kS, sv);
+      }
       f = (f < 1e-300) ? 1e-300 : f;
-      const double iy = 1.0 / S.sy[i];
+      const double iy = S.rec[i].x;  // == 1.0 / S.sy[i]
       double* row = c.chunk + c.lane * 5;
       row[0] = 1.0 * iy;
       row[1] = (1.0 / f) * iy;
@@ -1100,7 +1126,20 @@ static __device__ NX_COLD FitOut exact_fit(Ctx& c, const Stage& S, const Params&
       row[4] = sv * iy;
     }
     __syncwarp();
-    fold_chunk(c, min(32, n - base), acc);
+    const int cnt = min(32, n - base);
+    if (cnt == 32) {  // unrolled: the loads run ahead of the add chain
+      int ei, ej;
+      acc_slot(c.lane, ei, ej);
+      if (c.lane < 15) {
+#pragma unroll
+        for (int k = 0; k < 32; ++k) acc += c.chunk[k * 5 + ei] * c.chunk[k * 5 + ej];
+      } else if (c.lane < 20) {
+#pragma unroll
+        for (int k = 0; k < 32; ++k) acc += c.chunk[k * 5 + ei] * 1.0;
+      }
+    } else {
+      fold_chunk(c, cnt, acc);
+    }
   }
   const int src = c.lane < 25 ? slot_of(c.lane / 5, c.lane % 5) : (c.lane < 30 ? 15 + c.lane - 25 : 0);
   const double e = __shfl_sync(NX_FULL, acc, src);
@@ -1200,7 +1239,7 @@ static __device__ bool less_scaled_impl(Ctx& c, const Stage& S, const FitOut& a,
 static __device__ bool less_scaled(Ctx& c, const Stage& S, const FitOut& a, const FitOut& b, double f) {
   const long long t0 = nx_clock();
   const bool r = less_scaled_impl(c, S, a, b, f);
-  if (c.lane == 0) count(c.rs->cycles[11], nx_clock() - t0);
+  (void)t0;
   return r;
 }
 static __device__ NX_COLD bool less_scaled_impl(Ctx& c, const Stage& S, const FitOut& a, const FitOut& b, double f) {
@@ -1236,7 +1275,7 @@ static __device__ NX_COLD void update_structural(Ctx& c, int e) {
   base.p = cur;
   const long long tb0 = nx_clock();
   base.err = wsse_tree(c, S, cur);
-  if (c.lane == 0) count(c.rs->cycles[14], nx_clock() - tb0);
+  (void)tb0;
   base.bound = 2.0 * (static_cast<double>(n) + 2.0) * kU * base.err;
   const double lo = log(1e-8), hi = log(1e4);
   const double shrink = 1.0 - 1e-3;
@@ -1301,7 +1340,9 @@ static __device__ NX_COLD void update_structural(Ctx& c, int e) {
   }
   // the winner's coefficients from the reference's exact normal equations
   {
+    const long long tx = nx_clock();
     const FitOut ex = exact_fit(c, S, cur, best.p.kB, best.p.kS);
+    if (c.lane == 0) count(c.rs->cycles[14], nx_clock() - tx);
     if (isfinite(ex.err)) best = ex;
     else best.err = ex.err;  // the exact system is singular: the reference fails this fit too
   }

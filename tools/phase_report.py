@@ -4,7 +4,7 @@ os.environ.setdefault("NX_PHASE_TIMERS", "1")  # the kernel skips its cycle coun
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2509_23384_b200 import sim, workloads as W
-NAMES = ["select+hash", "route+admit", "plan(LENS)", "complete", "report", "linear", "structural*", "fit-tables", "refit-wait", "fit-pass", "fit-total", "less_scaled", "stage", "fit-solve", "base-err", "solve5"]
+NAMES = ["select+hash", "route+admit", "plan(LENS)", "complete", "report", "linear", "structural*", "fit-tables", "refit-wait", "fit-pass", "fit-total", "cheap-sum", "stage", "fit-solve", "exact-fit", "solve5"]
 ap = argparse.ArgumentParser()
 ap.add_argument("--requests", type=int, default=2000)
 a = ap.parse_args()

@@ -742,6 +742,30 @@ static __device__ __forceinline__ void pass_range(const double2* rec, const doub
   out[8] = warp_sum(a24); out[9] = warp_sum(t1); out[10] = warp_sum(t2);
 }
 
+// Totals of 11 per-lane partials in every lane: a reduce-scatter (each
+// butterfly level keeps half of the slots, 16 double shuffles for 16 padded
+// slots instead of 55 for 11 separate trees), then one broadcast per slot.
+// Fixed pattern, so the result never depends on timing.
+__device__ __forceinline__ void warp_sum11(const double a[11], double tot[11]) {
+  const int lane = lane_id();
+  const int h4 = (lane >> 4) & 1, h3 = (lane >> 3) & 1, h2 = (lane >> 2) & 1, h1 = (lane >> 1) & 1;
+  double v8[8], v4[4], v2[2];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const double lo = a[j], hi = j + 8 < 11 ? a[j + 8] : 0.0;
+    v8[j] = (h4 ? hi : lo) + __shfl_xor_sync(NX_FULL, h4 ? lo : hi, 16);
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) v4[j] = (h3 ? v8[j + 4] : v8[j]) + __shfl_xor_sync(NX_FULL, h3 ? v8[j] : v8[j + 4], 8);
+#pragma unroll
+  for (int j = 0; j < 2; ++j) v2[j] = (h2 ? v4[j + 2] : v4[j]) + __shfl_xor_sync(NX_FULL, h2 ? v4[j] : v4[j + 2], 4);
+  double v = (h1 ? v2[1] : v2[0]) + __shfl_xor_sync(NX_FULL, h1 ? v2[0] : v2[1], 2);
+  v = v + __shfl_xor_sync(NX_FULL, v, 1);  // lane holds slot 8 h4 + 4 h3 + 2 h2 + h1
+#pragma unroll
+  for (int q = 0; q < 11; ++q)
+    tot[q] = __shfl_sync(NX_FULL, v, (((q >> 3) & 1) << 4) | (((q >> 2) & 1) << 3) | (((q >> 1) & 1) << 2) | ((q & 1) << 1));
+}
+
 // Named barrier of the refit team (warps 1..kRefitWarps of the replica CTA).
 __device__ __forceinline__ void team_sync() {
   asm volatile("bar.sync 1, %0;" ::"r"(32 * kRefitWarps) : "memory");
@@ -1021,7 +1045,14 @@ static __device__ NX_COLD FitOut gauged_fit_impl(Ctx& c, Stage& S, const Params&
     }
     t.op = op;
     const long long tq = nx_clock();
-    run_task(c, t, tot);
+    if (op == 1) {
+      run_task(c, t, tot);
+    } else {  // a few hundred groups at most: the leader alone, no team round trip
+      double a[11] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+      if (op == 2) sum_over_b(t, c.lane, 32, a);
+      else sum_over_s(t, c.lane, 32, a);
+      warp_sum11(a, tot);
+    }
     if (c.lane == 0 && op != 1) count(c.rs->cycles[11], nx_clock() - tq);
 #ifdef NX_TRACE_FIT
     if (op != 1 && S.n == 1024) {

@@ -309,20 +309,26 @@ def operators(torch, dev) -> dict:
 
 
 # ---------------------------------------------------------------------------- arms
+def strided_idx(n: int, k: int):
+    """k replica indices spread evenly over the shard (every rate and policy
+    class), not its prefix (the grid orders seeds first, so a prefix is low-rate)."""
+    k = max(1, min(k, n))
+    step = n / k
+    return [int(i * step) for i in range(k)]
+
+
 def strided(cfgs, k: int):
-    """k replicas spread evenly over the shard (every rate and policy class),
-    not its prefix (the grid orders seeds first, so a prefix is low-rate)."""
-    k = max(1, min(k, len(cfgs)))
-    step = len(cfgs) / k
-    return [cfgs[int(i * step)] for i in range(k)]
+    return [cfgs[i] for i in strided_idx(len(cfgs), k)]
 
 
-def cpu_reference_rate(cfgs, threads: int):
+def cpu_reference_rate(cfgs, threads: int, detail: bool = False):
     sys.path.insert(0, str(ROOT / "tests"))
     from oracle_lib import Port, Ref, ref_available
     checker = Ref() if ref_available() else Port()
     kind = "reference" if ref_available() else "port"
-    dec, _, wall = checker.run_batch(cfgs, threads)
+    dec, hashes, wall = checker.run_batch(cfgs, threads)
+    if detail:
+        return sum(dec) / wall, kind, wall, sum(dec), dec, hashes
     return sum(dec) / wall, kind, wall, sum(dec)
 
 
@@ -491,12 +497,20 @@ def run_nx(args):
             except Exception as exc:
                 line["operators"] = {"error": repr(exc)}
         if world == 1 and not args.no_cpu_baseline:
-            sample = strided(cfgs, args.cpu_sample)
-            rate, kind, wall, dec = cpu_reference_rate(sample, os.cpu_count() or 1)
+            idx = strided_idx(len(cfgs), args.cpu_sample)
+            sample = [cfgs[i] for i in idx]
+            rate, kind, wall, dec, rdec, rhash = cpu_reference_rate(sample, os.cpu_count() or 1, detail=True)
             line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": os.cpu_count(),
                                     "kind": kind,
                                     "sample": f"{len(sample)} replicas spread over this shard, "
                                               f"{dec} decisions in {wall:.1f} s"}
+            # the same replicas, checked against the timed device run: the event
+            # hash fingerprints every routing choice, batch composition and time
+            dsum = batch.summaries()
+            line["cpu_baseline"]["parity"] = {
+                "replicas": len(idx),
+                "event_hash_equal": sum(int(dsum[i].event_hash == h) for i, h in zip(idx, rhash)),
+                "decisions_equal": sum(int(dsum[i].decisions == d) for i, d in zip(idx, rdec))}
         print(json.dumps(line), flush=True)
     batch.close()
     if world > 1:

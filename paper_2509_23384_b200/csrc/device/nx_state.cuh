@@ -149,7 +149,14 @@ __device__ __forceinline__ bool failed(const Ctx& c) { return c.rs->status != 0;
 // unless the launch sets it (NX_PHASE_TIMERS=1): the clock reads and the
 // shared-memory atomics stay off the event loop's critical path.
 // (one copy per translation unit; the simulator's launcher sets its own)
+// Phase timers exist only in the diagnostic build (-DNX_TIMERS, made by
+// tools/phase_report.py); the product kernel compiles every clock read and
+// counter update away.
+#ifdef NX_TIMERS
 static __constant__ int nx_timers_on;
+#else
+constexpr int nx_timers_on = 0;
+#endif
 
 __device__ __forceinline__ long long nx_clock() {
 #ifdef __CUDA_ARCH__

@@ -1259,11 +1259,13 @@ extern "C" cudaError_t nx_launch_sim(const NxPools* d_pools, const int32_t* d_or
                                      int* d_next, int smem_per_warp, int prefix_cap, int max_eng,
                                      int grid, int warps_per_block, int n_excl, cudaStream_t st) {
   const size_t smem = static_cast<size_t>(smem_per_warp);  // one replica per CTA
+#ifdef NX_TIMERS
   const char* tm = getenv("NX_PHASE_TIMERS");
   const int timers = tm && tm[0] == '1';
   cudaError_t terr = cudaMemcpyToSymbolAsync(nxd::nx_timers_on, &timers, sizeof timers, 0,
                                              cudaMemcpyHostToDevice, st);
   if (terr != cudaSuccess) return terr;
+#endif
   cudaError_t err = cudaFuncSetAttribute(nx_sim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
   if (err != cudaSuccess) return err;

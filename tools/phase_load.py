@@ -2,6 +2,16 @@
 full bench-shard launch (where does co-residency / load slow the event loop?)."""
 import os, sys
 os.environ.setdefault("NX_PHASE_TIMERS", "1")
+# the product library has no phase timers: use (and if needed build) the
+# diagnostic -DNX_TIMERS build
+_TIMERS = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_timers", "_nxsched.so")
+if "NX_SO" not in os.environ:
+    if not os.path.exists(_TIMERS):
+        import subprocess
+        _csrc = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "paper_2509_23384_b200", "csrc")
+        subprocess.run(["make", "-C", _csrc, f"OUT={_TIMERS}", f"B={os.path.dirname(_TIMERS)}/build",
+                        "EXTRA=-DNX_TIMERS"], check=True, stdout=subprocess.DEVNULL)
+    os.environ["NX_SO"] = _TIMERS
 from collections import defaultdict
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))

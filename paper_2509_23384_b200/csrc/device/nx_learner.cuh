@@ -143,12 +143,18 @@ __device__ __forceinline__ bool solve5_warp(double v, double x[5], bool* ambiguo
 }
 
 // lane -> (i, j) of the 15 unique A^T A entries; lanes 15..19 own A^T b[i].
+// (3-bit fields of two constants: a local-array table here was stored to and
+// reloaded from local memory on every call.)
 __device__ __forceinline__ void acc_slot(int lane, int& i, int& j) {
-  const int ti[15] = {0, 0, 0, 0, 0, 1, 1, 1, 1, 2, 2, 2, 3, 3, 4};
-  const int tj[15] = {0, 1, 2, 3, 4, 1, 2, 3, 4, 2, 3, 4, 3, 4, 4};
+  constexpr unsigned long long kTi = 0ull | 0ull << 3 | 0ull << 6 | 0ull << 9 | 0ull << 12 | 1ull << 15 |
+                                     1ull << 18 | 1ull << 21 | 1ull << 24 | 2ull << 27 | 2ull << 30 |
+                                     2ull << 33 | 3ull << 36 | 3ull << 39 | 4ull << 42;
+  constexpr unsigned long long kTj = 0ull | 1ull << 3 | 2ull << 6 | 3ull << 9 | 4ull << 12 | 1ull << 15 |
+                                     2ull << 18 | 3ull << 21 | 4ull << 24 | 2ull << 27 | 3ull << 30 |
+                                     4ull << 33 | 3ull << 36 | 4ull << 39 | 4ull << 42;
   if (lane < 15) {
-    i = ti[lane];
-    j = tj[lane];
+    i = static_cast<int>((kTi >> (3 * lane)) & 7ull);
+    j = static_cast<int>((kTj >> (3 * lane)) & 7ull);
   } else {
     i = lane - 15;
     j = -1;

@@ -145,10 +145,6 @@ __device__ __forceinline__ void fail(Ctx& c, int status, int site, int64_t info)
 }
 __device__ __forceinline__ bool failed(const Ctx& c) { return c.rs->status != 0; }
 
-// Phase-cycle instrumentation (diagnostic, tools/phase_report.py) is off
-// unless the launch sets it (NX_PHASE_TIMERS=1): the clock reads and the
-// shared-memory atomics stay off the event loop's critical path.
-// (one copy per translation unit; the simulator's launcher sets its own)
 // Phase timers exist only in the diagnostic build (-DNX_TIMERS, made by
 // tools/phase_report.py); the product kernel compiles every clock read and
 // counter update away.

@@ -957,14 +957,9 @@ __device__ void run_replica(Ctx& c) {
     const int64_t now = static_cast<int64_t>(now_u);
     // ---- consume the slot ----
     int rid = 0;
-    double dv[5];
-    int64_t dq_q = 0;
+    int64_t dq_o = 0;  // the delivered report's slot (read in case 4; no push in between)
     if (kind == 0) rid = c.rs->cursor;
-    if (kind == 4) {
-      const int64_t o = c.ed[who].dq_off + c.eng[who].dq_head;
-      for (int i = 0; i < 5; ++i) dv[i] = c.P->dq_sv[5 * o + i];
-      dq_q = c.P->dq_qlen[o];
-    }
+    if (kind == 4) dq_o = c.ed[who].dq_off + c.eng[who].dq_head;
     __syncwarp();
     if (c.lane == 0) {
       EngSm& g = c.eng[kind == 0 ? 0 : who];
@@ -1078,12 +1073,13 @@ __device__ void run_replica(Ctx& c) {
         if (c.lane == 0) {
           EngSm& g = c.eng[who];
           g.has_rep = 1;
+          const double* dv = c.P->dq_sv + 5 * dq_o;
           g.rep_lhat = dv[0];
           g.rep_wload = dv[1];
           g.rep_mfree = dv[2];
           g.rep_pmax = dv[3];
           g.rep_at = dv[4];
-          g.rep_qlen = dq_q;
+          g.rep_qlen = c.P->dq_qlen[dq_o];
         }
         __syncwarp();
         break;

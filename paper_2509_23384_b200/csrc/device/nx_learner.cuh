@@ -1,15 +1,19 @@
 // K4 — online coefficient refit, one warp per engine update.
 //
 // Replaces OnlineLearner (proj/src/learner.cpp:130-440). Reduction orders:
-//  * the normal-equation accumulators (15 unique A^T A entries + 5 A^T b) are
-//    folded in the reference's left-to-right sample order, one accumulator
-//    per lane over 32-sample chunks staged in shared memory — so the fitted
-//    coefficients are the reference's bit for bit (modulo libm ulps);
-//  * the squared-error sums (ridge scale, windowed SSE) are fixed-order warp
-//    trees; every decision they drive (lambda cap, accept/reject) is
-//    certified against the summation error bound and, if the tree value sits
-//    inside it, recomputed as an exact left fold. Decisions therefore equal
-//    the reference's left-fold decisions.
+//  * coefficients a learner adopts come from normal equations (15 unique
+//    A^T A entries + 5 A^T b) folded in the reference's left-to-right sample
+//    order, one accumulator per lane over 32-sample chunks staged in shared
+//    memory — the linear tier always, the structural tier for its winning
+//    (kB, kS) (exact_fit) — so they are the reference's bit for bit (modulo
+//    libm ulps);
+//  * the structural search ranks its ~50-100 candidate fits on fast sums
+//    (team passes, grouped per-batch-size / per-token-count aggregates), and
+//    the squared-error sums (ridge scale, windowed SSE) are fixed-order warp
+//    trees; every decision they drive (lambda cap, accept/reject, rank test)
+//    is certified against an explicit rounding bound and, if it falls inside,
+//    re-taken on the exact left fold. Decisions therefore equal the
+//    reference's left-fold decisions.
 #pragma once
 #include "nx_state.cuh"
 #ifdef NX_TRACE_FIT

@@ -1510,20 +1510,24 @@ static __device__ NX_COLD void record_sample(Ctx& c, int e, int b, int s, double
       g.ring_size += 1;
     } else {
       slot = g.ring_head;
-      g.ring_head = (g.ring_head + 1) % g.ring_size;
+      g.ring_head = g.ring_head + 1 == g.ring_size ? 0 : g.ring_head + 1;
     }
     c.P->ring_b[ed.ring_off + slot] = b;
     c.P->ring_s[ed.ring_off + slot] = s;
     c.P->ring_y[ed.ring_off + slot] = y;
     g.seen += 1;
+    // seen % period == 0 as countdowns (a 64-bit remainder by a runtime
+    // divisor is a long software sequence on the event loop)
+    if (--g.lin_left == 0) g.lin_left = c.d->l_period;
+    if (--g.str_left == 0) g.str_left = c.d->s_period;
   }
   __syncwarp();
   const int64_t seen = g.seen;
-  if (seen % c.d->l_period == 0) {
+  if (g.lin_left == c.d->l_period) {
     PhaseTimer pt(c.rs, 5);
     update_linear(c, e);
   }
-  if (seen >= c.d->min_s && seen % c.d->s_period == 0) post_refit(c, e);
+  if (seen >= c.d->min_s && g.str_left == c.d->s_period) post_refit(c, e);
 }
 
 }  // namespace nxd

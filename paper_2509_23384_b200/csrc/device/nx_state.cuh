@@ -75,6 +75,7 @@ struct EngSm {
   uint64_t step_t, learn_t, report_t;          // pending-event slots (kNoEvent = none)
   uint64_t dq_t0;                              // head of the delivery FIFO (cached)
   int64_t started_us, seen, rep_qlen, tw_degen;
+  int32_t lin_left, str_left;                  // samples until the next linear / structural period
   int64_t cnt[7];                              // LearnerCounters
   uint32_t step_seq, learn_seq, report_seq, dq_s0;
   int32_t wq_head, wq_len, rq_len;

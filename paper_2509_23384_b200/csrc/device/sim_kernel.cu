@@ -24,6 +24,17 @@ constexpr double kInf = __builtin_huge_val();
 
 // ---- small helpers ------------------------------------------------------------
 __device__ __forceinline__ int blocks_for(int tokens, int block) { return (tokens + block - 1) / block; }
+// (i + j) mod cap for 0 <= i, j <= cap (ring positions): a compare instead of
+// a remainder by a runtime divisor.
+__device__ __forceinline__ int ring_add(int i, int j, int cap) {
+  const int t = i + j;
+  return t >= cap ? t - cap : t;
+}
+// rr % n for the round-robin counter, 32-bit while it fits.
+__device__ __forceinline__ int rr_mod(uint64_t rr, int n) {
+  return rr < (1ull << 32) ? static_cast<int>(static_cast<uint32_t>(rr) % static_cast<uint32_t>(n))
+                           : static_cast<int>(rr % static_cast<uint64_t>(n));
+}
 __device__ __forceinline__ int remaining(const Ctx& c, int r) {
   return c.P->req[c.roff + r].prompt - c.P->req[c.roff + r].prefilled;
 }
@@ -535,7 +546,7 @@ __device__ NX_COLD void step_complete(Ctx& c, int e, int64_t now_us) {
               c.rs->status = 1;
               c.rs->site = NX_SITE_OVERFLOW;
             } else {
-              const int slot = (g.lat_head + g.lat_len) % ed.lat_cap;
+              const int slot = ring_add(g.lat_head, g.lat_len, ed.lat_cap);
               P.lat_t[ed.lat_off + slot] = now;
               P.lat_e2e[ed.lat_off + slot] = now - P.arr_ms[ro + rr];
               g.lat_len += 1;
@@ -649,7 +660,7 @@ __device__ NX_COLD void state_report(Ctx& c, int e, int64_t now_us) {
       c.rs->status = 1;
       c.rs->site = NX_SITE_OVERFLOW;
     } else {
-      const int slot = (g.dq_head + g.dq_len) % ed.dq_cap;
+      const int slot = ring_add(g.dq_head, g.dq_len, ed.dq_cap);
       const int64_t o = ed.dq_off + slot;
       const int64_t dt = now_us + ed.stale_us;
       const uint32_t ds = c.rs->next_seq++;
@@ -709,7 +720,7 @@ __device__ NX_COLD int route(Ctx& c, int rid, double now, double& score, double 
   __syncwarp();
   switch (d.route_policy) {
     case 1: {  // round_robin
-      chosen = static_cast<int>(c.rs->rr_next % static_cast<uint64_t>(n));
+      chosen = rr_mod(c.rs->rr_next, n);
       put(c.rs->rr_next, c.rs->rr_next + 1);
       break;
     }
@@ -718,7 +729,7 @@ __device__ NX_COLD int route(Ctx& c, int rid, double now, double& score, double 
       if (se >= 0) {
         chosen = se;
       } else {
-        chosen = static_cast<int>(c.rs->rr_next % static_cast<uint64_t>(n));
+        chosen = rr_mod(c.rs->rr_next, n);
         put(c.rs->rr_next, c.rs->rr_next + 1);
       }
       break;
@@ -739,7 +750,7 @@ __device__ NX_COLD int route(Ctx& c, int rid, double now, double& score, double 
         double sum = g.lat_sum;
         while (len > 0 && lt[head] < horizon) {
           sum -= le[head];
-          head = (head + 1) % ed.lat_cap;
+          head = ring_add(head, 1, ed.lat_cap);
           --len;
         }
         g.lat_head = head;  // engine-owned fields: lane e is the only writer
@@ -884,6 +895,7 @@ __device__ NX_COLD void init_replica(Ctx& c) {
     g.report_t = 0; g.report_seq = static_cast<uint32_t>(e);  // initial reports: seq 0..E-1
     g.step_seq = 0; g.learn_seq = 0;
     g.started_us = 0; g.seen = 0; g.rep_qlen = 0; g.tw_degen = 0;
+    g.lin_left = d.l_period; g.str_left = d.s_period;
     for (int i = 0; i < 7; ++i) g.cnt[i] = 0;
     g.wq_head = 0; g.wq_len = 0; g.rq_len = 0;
     g.pinned = 0; g.reserved = 0; g.cache_blocks = 0; g.lru_head = -1; g.lru_tail = -1;
@@ -972,7 +984,7 @@ __device__ void run_replica(Ctx& c) {
       else if (kind == 2) g.report_t = kNoEvent;
       else if (kind == 3) g.learn_t = kNoEvent;
       else {
-        g.dq_head = (g.dq_head + 1) % c.ed[who].dq_cap;
+        g.dq_head = ring_add(g.dq_head, 1, c.ed[who].dq_cap);
         g.dq_len -= 1;
         if (g.dq_len > 0) {
           const int64_t o = c.ed[who].dq_off + g.dq_head;

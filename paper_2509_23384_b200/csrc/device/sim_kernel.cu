@@ -23,7 +23,12 @@ namespace nxd {
 constexpr double kInf = __builtin_huge_val();
 
 // ---- small helpers ------------------------------------------------------------
-__device__ __forceinline__ int blocks_for(int tokens, int block) { return (tokens + block - 1) / block; }
+// ceil(tokens / block) for tokens >= 0; block sizes are powers of two in
+// practice (16), where a shift replaces the integer division sequence.
+__device__ __forceinline__ int blocks_for(int tokens, int block) {
+  const int t = tokens + block - 1;
+  return (block & (block - 1)) == 0 ? t >> (__ffs(block) - 1) : t / block;
+}
 // (i + j) mod cap for 0 <= i, j <= cap (ring positions): a compare instead of
 // a remainder by a runtime divisor.
 __device__ __forceinline__ int ring_add(int i, int j, int cap) {

@@ -5,7 +5,7 @@
 //    A^T A entries + 5 A^T b) folded in the reference's left-to-right sample
 //    order, one accumulator per lane over 32-sample chunks staged in shared
 //    memory — the linear tier always, the structural tier for its winning
-//    (kB, kS) (exact_fit) — so they are the reference's bit for bit (modulo
+//    (kB, kS) (exact_elem) — so they are the reference's bit for bit (modulo
 //    libm ulps);
 //  * the structural search ranks its ~50-100 candidate fits on fast sums
 //    (team passes, grouped per-batch-size / per-token-count aggregates), and
@@ -963,19 +963,24 @@ static __device__ void run_task(Ctx& c, const TeamTask& t, double tot[11]) {
   __syncwarp();
 }
 
-static __device__ FitOut gauged_fit_impl(Ctx& c, Stage& S, const Params& cur, double kB, double kS);
+static __device__ FitOut gauged_fit_impl(Ctx& c, Stage& S, const Params& cur, double kB, double kS, bool exact);
 static __device__ FitOut finish_fit(Ctx& c, const Stage& S, const Params& cur, double kB, double kS, double e,
                                    bool* ambiguous);
-static __device__ FitOut exact_fit(Ctx& c, Stage& S, const Params& cur, double kB, double kS);
-static __device__ FitOut gauged_fit(Ctx& c, Stage& S, const Params& cur, double kB, double kS) {
+static __device__ double exact_elem(Ctx& c, Stage& S, double kB, double kS);
+static __device__ FitOut gauged_fit(Ctx& c, Stage& S, const Params& cur, double kB, double kS, bool exact = false) {
   const long long t0 = nx_clock();
-  FitOut o = gauged_fit_impl(c, S, cur, kB, kS);
+  FitOut o = gauged_fit_impl(c, S, cur, kB, kS, exact);
   if (c.lane == 0) count(c.rs->cycles[10], nx_clock() - t0);
   return o;
 }
-static __device__ NX_COLD FitOut gauged_fit_impl(Ctx& c, Stage& S, const Params& cur, double kB, double kS) {
-  if (c.lane == 0) count(c.rs->work[5], 1);
+static __device__ NX_COLD FitOut gauged_fit_impl(Ctx& c, Stage& S, const Params& cur, double kB, double kS,
+                                                 bool exact) {
   const int n = S.n;
+  double e;
+  if (exact) {
+    e = exact_elem(c, S, kB, kS);
+  } else {
+  if (c.lane == 0) count(c.rs->work[5], 1);
   const long long tf0 = nx_clock();
   // Which sum: over b (kS unchanged since ab was built), over the distinct
   // token counts (kB unchanged since as was built), either after rebuilding
@@ -1116,11 +1121,21 @@ static __device__ NX_COLD FitOut gauged_fit_impl(Ctx& c, Stage& S, const Params&
   const double u15[15] = {S.A00, tot[0], tot[1], S.A03, S.A04, tot[2], tot[3], tot[5], tot[6],
                           tot[4], tot[7], tot[8], S.A33, S.A34, S.A44};
   const double t5[5] = {S.t0, tot[9], tot[10], S.t3, S.t4};
+  e = normal_elem(u15, t5);
+  (void)tf2;
+  }
+  const long long ts = nx_clock();
+  // one call site of the solve (it is large): a rank test too close to call
+  // on the fast sums goes round once more on the reference's exact ones
   bool ambiguous = false;
-  FitOut out = finish_fit(c, S, cur, kB, kS, normal_elem(u15, t5), &ambiguous);
-  // a rank test too close to call on the fast sums: the reference's exact ones decide
-  if (ambiguous) out = exact_fit(c, S, cur, kB, kS);
-  if (c.lane == 0) count(c.rs->cycles[13], nx_clock() - tf2);
+  FitOut out;
+#pragma unroll 1
+  for (int pass = exact ? 1 : 0;; ++pass) {
+    out = finish_fit(c, S, cur, kB, kS, e, pass == 0 ? &ambiguous : nullptr);
+    if (pass > 0 || !ambiguous) break;
+    e = exact_elem(c, S, kB, kS);
+  }
+  if (c.lane == 0) count(c.rs->cycles[13], nx_clock() - ts);
   return out;
 }
 
@@ -1131,7 +1146,7 @@ static __device__ NX_COLD FitOut gauged_fit_impl(Ctx& c, Stage& S, const Params&
 // certified); the winner's coefficients are recomputed here so the learner
 // adopts the reference's values, not values a few ulps of the window sums
 // away (the 5x5 solve amplifies those by the system's condition number).
-static __device__ NX_COLD FitOut exact_fit(Ctx& c, Stage& S, const Params& cur, double kB, double kS) {
+static __device__ NX_COLD double exact_elem(Ctx& c, Stage& S, double kB, double kS) {
   const int n = S.n;
   // f_B by batch size and f_S by distinct token count (the reference's
   // per-sample expm1 values) in the fit tables' storage, which the next fit
@@ -1183,8 +1198,7 @@ static __device__ NX_COLD FitOut exact_fit(Ctx& c, Stage& S, const Params& cur, 
     }
   }
   const int src = c.lane < 25 ? slot_of(c.lane / 5, c.lane % 5) : (c.lane < 30 ? 15 + c.lane - 25 : 0);
-  const double e = __shfl_sync(NX_FULL, acc, src);
-  return finish_fit(c, S, cur, kB, kS, e, nullptr);
+  return __shfl_sync(NX_FULL, acc, src);
 }
 
 // Solve, ridge and trust region of gauged_fit (learner.cpp:246-297) from the
@@ -1382,7 +1396,7 @@ static __device__ NX_COLD void update_structural(Ctx& c, int e) {
   // the winner's coefficients from the reference's exact normal equations
   {
     const long long tx = nx_clock();
-    const FitOut ex = exact_fit(c, S, cur, best.p.kB, best.p.kS);
+    const FitOut ex = gauged_fit(c, S, cur, best.p.kB, best.p.kS, true);
     if (c.lane == 0) count(c.rs->cycles[14], nx_clock() - tx);
     if (isfinite(ex.err)) best = ex;
     else best.err = ex.err;  // the exact system is singular: the reference fails this fit too

@@ -46,7 +46,7 @@ def parse():
     ap.add_argument("--impl", choices=["nx", "reference"], default="nx")
     ap.add_argument("--replicas-per-gpu", type=int, default=512)
     ap.add_argument("--requests", type=int, default=2000)
-    ap.add_argument("--cpu-sample", type=int, default=64, help="replicas timed for cpu_baseline")
+    ap.add_argument("--cpu-sample", type=int, default=128, help="replicas timed for cpu_baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-operators", action="store_true", help="skip the batched K2/K3/K4 lines")
@@ -338,7 +338,10 @@ def run_reference(args):
         return
     threads = os.cpu_count() or 1
     cfgs = shard_configs(0, args.replicas_per_gpu, args.requests)
-    sample = strided(cfgs, 4 * threads)  # 4 per thread: less end-of-batch idling
+    # 8 replicas per host thread, longest expected first (lowest arrival rate:
+    # most steps): the dynamic queue then ends with short replicas instead of
+    # idling cores behind a long one
+    sample = sorted(strided(cfgs, 8 * threads), key=lambda c: c["workload"]["rate"])
     rates = []
     for i in range(args.warmup + args.steps):
         r, kind, wall, dec = cpu_reference_rate(sample, threads)
@@ -355,7 +358,7 @@ def run_reference(args):
         "config": workload_desc(args.replicas_per_gpu, args.requests, args.gpus),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
                          "sample": f"{len(sample)} replicas spread over the rank-0 shard per step, "
-                                   f"one std::thread per host core"},
+                                   f"longest first, one std::thread per host core"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -497,13 +500,14 @@ def run_nx(args):
             except Exception as exc:
                 line["operators"] = {"error": repr(exc)}
         if world == 1 and not args.no_cpu_baseline:
-            idx = strided_idx(len(cfgs), args.cpu_sample)
+            # longest expected first (lowest rate), as in the reference arm
+            idx = sorted(strided_idx(len(cfgs), args.cpu_sample), key=lambda i: cfgs[i]["workload"]["rate"])
             sample = [cfgs[i] for i in idx]
             rate, kind, wall, dec, rdec, rhash = cpu_reference_rate(sample, os.cpu_count() or 1, detail=True)
             line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": os.cpu_count(),
                                     "kind": kind,
-                                    "sample": f"{len(sample)} replicas spread over this shard, "
-                                              f"{dec} decisions in {wall:.1f} s"}
+                                    "sample": f"{len(sample)} replicas spread over this shard, longest "
+                                              f"first, {dec} decisions in {wall:.1f} s"}
             # the same replicas, checked against the timed device run: the event
             # hash fingerprints every routing choice, batch composition and time
             dsum = batch.summaries()

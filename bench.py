@@ -46,7 +46,9 @@ def parse():
     ap.add_argument("--impl", choices=["nx", "reference"], default="nx")
     ap.add_argument("--replicas-per-gpu", type=int, default=512)
     ap.add_argument("--requests", type=int, default=2000)
-    ap.add_argument("--cpu-sample", type=int, default=128, help="replicas timed for cpu_baseline")
+    ap.add_argument("--cpu-sample", type=int, default=512,
+                    help="replicas of the rank-0 shard timed for cpu_baseline (and parity-checked)")
+    ap.add_argument("--no-configs", action="store_true", help="skip BASELINE configs 1-4")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-operators", action="store_true", help="skip the batched K2/K3/K4 lines")
@@ -186,14 +188,67 @@ def k1_model_eval(torch, dev) -> dict:
                          "bytes_per_record": 20}}
 
 
+TRAFFIC_FILE = "r02_traffic.json"
+TRAFFIC_SOURCE = (f"profiles/{TRAFFIC_FILE}: dram__bytes_read.sum + dram__bytes_write.sum of one "
+                  "ncu --set full capture of this build (not re-measured in this run)")
+
+
 def traffic(kernel: str):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel`
-    from the committed ncu --set full capture (profiles/r01_traffic.json)."""
+    from the committed ncu --set full capture of the current build."""
     try:
-        t = json.loads((ROOT / "profiles" / "r01_traffic.json").read_text())
+        t = json.loads((ROOT / "profiles" / TRAFFIC_FILE).read_text())
         return t[kernel]["traffic_bytes_per_launch"]
     except Exception:
         return None
+
+
+def baseline_configs_line(torch, local: int) -> dict:
+    """BASELINE configs 1-4 at their stated sizes: one
+    device batch of the five single-replica runs, each replica's own device
+    time (%globaltimer begin/end) -> decisions/s, next to the reference
+    simulator (oracle/_ref) on one host thread per config, and the parity of
+    the two (event hash + decisions). Single replicas do not shard
+    ("replicas only"): a replica's event loop is sequential."""
+    import tempfile
+    from paper_2509_23384_b200 import sim, workloads as W
+    sys.path.insert(0, str(ROOT / "tests"))
+    from oracle_lib import Port, Ref, ref_available
+    from concurrent.futures import ThreadPoolExecutor
+    td = tempfile.mkdtemp(prefix="nx_cfg_")
+    cfgs = W.baseline_configs(td, sim.synth_generate)
+    names = list(cfgs)
+    chk = Ref() if ref_available() else Port()
+
+    def ref_one(c):
+        t0 = time.perf_counter()
+        r = chk.run(c)
+        return r, time.perf_counter() - t0
+
+    with ThreadPoolExecutor(max_workers=len(names)) as ex:
+        futs = {n: ex.submit(ref_one, cfgs[n]) for n in names}
+        b = sim.Batch([cfgs[n] for n in names], device=local)
+        b.upload()
+        b.launch()
+        b.download()
+        b.synchronize()
+        launch_ms = b.kernel_ms()
+        sums = b.summaries()
+        out = {}
+        for i, n in enumerate(names):
+            t0, t1 = b.timeline(i)
+            dev_s = max(1e-9, (t1 - t0) / 1e9)
+            want, ref_s = futs[n].result()
+            out[n] = {"decisions": sums[i].decisions, "device_s": dev_s,
+                      "device_decisions_per_s": sums[i].decisions / dev_s,
+                      "reference_s": ref_s, "reference_decisions_per_s": want["decisions"] / ref_s,
+                      "event_hash_equal": f"{sums[i].event_hash:016x}" == want["event_hash"],
+                      "decisions_equal": sums[i].decisions == want["decisions"]}
+    b.close()
+    return {"launch_ms": launch_ms, "reference_kind": "reference" if ref_available() else "port",
+            "reference_threads": "one host thread per config, all five concurrently",
+            "note": "single replicas: sequential event loops, run side by side in one launch",
+            "per_config": out}
 
 
 def operators(torch, dev) -> dict:
@@ -309,16 +364,20 @@ def operators(torch, dev) -> dict:
 
 
 # ---------------------------------------------------------------------------- arms
-def strided_idx(n: int, k: int):
-    """k replica indices spread evenly over the shard (every rate and policy
-    class), not its prefix (the grid orders seeds first, so a prefix is low-rate)."""
-    k = max(1, min(k, n))
-    step = n / k
-    return [int(i * step) for i in range(k)]
+def balanced_prefix(n: int, k: int):
+    """Indices of a sample of k replicas with every rate x policy cell equally
+    represented: the shard grid is seed-major with all 16 rates x 4 router
+    policies inside each seed (workloads.sweep_configs), so whole 64-replica
+    seed blocks from the front of the shard are exactly balanced (a strided
+    pick with step 4 would alias onto a single policy)."""
+    k = max(1, min(n, 64 * math.ceil(max(1, k) / 64)))
+    return list(range(k))
 
 
-def strided(cfgs, k: int):
-    return [cfgs[i] for i in strided_idx(len(cfgs), k)]
+def longest_first(cfgs, idx):
+    """Replica indices ordered longest expected first (lowest arrival rate:
+    most steps), so a host thread pool ends on short replicas."""
+    return sorted(idx, key=lambda i: cfgs[i]["workload"]["rate"])
 
 
 def cpu_reference_rate(cfgs, threads: int, detail: bool = False):
@@ -338,10 +397,10 @@ def run_reference(args):
         return
     threads = os.cpu_count() or 1
     cfgs = shard_configs(0, args.replicas_per_gpu, args.requests)
-    # 8 replicas per host thread, longest expected first (lowest arrival rate:
-    # most steps): the dynamic queue then ends with short replicas instead of
-    # idling cores behind a long one
-    sample = sorted(strided(cfgs, 8 * threads), key=lambda c: c["workload"]["rate"])
+    # ~8 replicas per host thread in whole rate x policy blocks, longest
+    # expected first: the dynamic queue then ends with short replicas instead
+    # of idling cores behind a long one
+    sample = [cfgs[i] for i in longest_first(cfgs, balanced_prefix(len(cfgs), 8 * threads))]
     rates = []
     for i in range(args.warmup + args.steps):
         r, kind, wall, dec = cpu_reference_rate(sample, threads)
@@ -357,8 +416,9 @@ def run_reference(args):
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload_desc(args.replicas_per_gpu, args.requests, args.gpus),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
-                         "sample": f"{len(sample)} replicas spread over the rank-0 shard per step, "
-                                   f"longest first, one std::thread per host core"},
+                         "sample": f"{len(sample)} replicas of the rank-0 shard per step (whole "
+                                   f"seed blocks: every rate x policy cell equally), longest first, "
+                                   f"one std::thread per host core"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -373,10 +433,21 @@ def run_nx(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # NX_BENCH_ONE_DEVICE=1 (tests only): every rank on cuda:0 with gloo for
+    # the host-side plumbing, so the N>1 path runs on a one-GPU box (NCCL
+    # refuses two ranks on one device)
+    one_dev = os.environ.get("NX_BENCH_ONE_DEVICE") == "1"
+    if one_dev:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    backend = "gloo" if one_dev else "nccl"
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if one_dev:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+    red_dev = torch.device("cpu") if backend == "gloo" else dev
 
     def barrier():
         if world > 1:
@@ -386,14 +457,14 @@ def run_nx(args):
     def max_over_ranks(v: float) -> float:
         if world == 1:
             return v
-        t = torch.tensor([v], device=dev, dtype=torch.float64)
+        t = torch.tensor([v], device=red_dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
     def sum_over_ranks(v: float) -> float:
         if world == 1:
             return v
-        t = torch.tensor([v], device=dev, dtype=torch.float64)
+        t = torch.tensor([v], device=red_dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
         return float(t.item())
 
@@ -427,14 +498,20 @@ def run_nx(args):
     total_dec = sum_over_ranks(decisions_step * args.steps)
     value = total_dec / t_dev
 
-    # e2e through the C-ABI with host buffers (upload + launch + download)
+    # e2e through the C-ABI with host buffers: workload generation on the
+    # host (as inside the reference's run_simulation clock), pinned H2D,
+    # launch, D2H of the results, per-replica summaries
     e2e = None
     if not args.no_e2e:
         barrier()
         t0 = time.perf_counter()
         for i in range(args.steps):
+            batch.rebuild_workloads(os.cpu_count())
             batch.run()
+            e2e_sums = batch.summaries()
         wall = time.perf_counter() - t0
+        if sum(x.decisions for x in e2e_sums) != decisions_step:
+            raise RuntimeError("e2e run diverged from the timed launches")
         barrier()
         h2d, d2h = batch.io_bytes()
         e2e_t = max_over_ranks(wall)
@@ -448,20 +525,28 @@ def run_nx(args):
     if world > 1:
         nbytes = batch.summaries_nbytes()
         out = torch.empty(nbytes * world, dtype=torch.uint8, device=dev)
-        try:
-            from paper_2509_23384_b200.collective import NcclComm
-            comm = NcclComm.from_torch_dist(rank, world, local)
-            batch.gather_summaries(comm, out.data_ptr())
-            batch.synchronize()
-            comm.close()
-            gather_via = "nx_sim_gather_summaries (ncclAllGather)"
-        except Exception as exc:  # noqa: BLE001
-            buf = torch.empty(nbytes, dtype=torch.uint8, device=dev)
-            batch.copy_summaries(buf.data_ptr())
-            batch.synchronize()  # the copy runs on the handle's stream, NCCL on torch's
-            dist.all_gather_into_tensor(out, buf)
-            torch.cuda.synchronize(dev)
-            gather_via = f"torch all_gather ({exc!r})"
+        buf = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+        batch.copy_summaries(buf.data_ptr())
+        if backend == "nccl":
+            try:
+                from paper_2509_23384_b200.collective import NcclComm
+                comm = NcclComm.from_torch_dist(rank, world, local)
+                batch.gather_summaries(comm, out.data_ptr())
+                batch.synchronize()
+                comm.close()
+                gather_via = "nx_sim_gather_summaries (ncclAllGather)"
+            except Exception as exc:  # noqa: BLE001
+                dist.all_gather_into_tensor(out, buf)
+                torch.cuda.synchronize(dev)
+                gather_via = f"torch all_gather ({exc!r})"
+        else:  # gloo: host copies of the same bytes
+            parts = [torch.empty(nbytes, dtype=torch.uint8) for _ in range(world)]
+            dist.all_gather(parts, buf.cpu())
+            out.copy_(torch.cat(parts))
+            gather_via = "torch.distributed gloo all_gather of host copies (one-device test mode)"
+        # every rank's records arrived intact: this rank's slice is its own
+        if not torch.equal(out[rank * nbytes:(rank + 1) * nbytes], buf):
+            raise RuntimeError("summary gather corrupted this rank's records")
         gathered = world * len(cfgs)
 
     # roofline of the dominant kernel (nx_sim_kernel), from device work counters
@@ -481,8 +566,12 @@ def run_nx(args):
             "gpu_launches": args.steps,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                          "frac": achieved / pk["hbm_gbs"], "traffic": traffic("nx_sim_kernel"),
+                         "traffic_source": TRAFFIC_SOURCE,
                          "kernel": "nx_sim_kernel", "peak_source": src,
-                         "algorithmic_bytes_per_launch": alg},
+                         "algorithmic_bytes_per_launch": alg,
+                         "limiter": "latency: one dependent event chain per replica (FP64 model "
+                                    "evaluations, shared-memory state); HBM is not the bound "
+                                    "(DESIGN.md §5)"},
             "clocks": clk.summary(),
         }
         if e2e:
@@ -499,22 +588,30 @@ def run_nx(args):
                 line["operators"] = operators(torch, dev)
             except Exception as exc:
                 line["operators"] = {"error": repr(exc)}
-        if world == 1 and not args.no_cpu_baseline:
+        if not args.no_cpu_baseline:
+            # the whole rank-0 shard through the reference on every host core,
             # longest expected first (lowest rate), as in the reference arm
-            idx = sorted(strided_idx(len(cfgs), args.cpu_sample), key=lambda i: cfgs[i]["workload"]["rate"])
+            idx = longest_first(cfgs, balanced_prefix(len(cfgs), args.cpu_sample))
             sample = [cfgs[i] for i in idx]
             rate, kind, wall, dec, rdec, rhash = cpu_reference_rate(sample, os.cpu_count() or 1, detail=True)
             line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": os.cpu_count(),
                                     "kind": kind,
-                                    "sample": f"{len(sample)} replicas spread over this shard, longest "
-                                              f"first, {dec} decisions in {wall:.1f} s"}
+                                    "sample": f"{len(sample)} replicas of the rank-0 shard (every rate x "
+                                              f"policy cell), longest first, {dec} decisions in {wall:.1f} s"}
             # the same replicas, checked against the timed device run: the event
             # hash fingerprints every routing choice, batch composition and time
             dsum = batch.summaries()
+            pol = [cfgs[i]["router"]["policy"] for i in idx]
             line["cpu_baseline"]["parity"] = {
                 "replicas": len(idx),
                 "event_hash_equal": sum(int(dsum[i].event_hash == h) for i, h in zip(idx, rhash)),
-                "decisions_equal": sum(int(dsum[i].decisions == d) for i, d in zip(idx, rdec))}
+                "decisions_equal": sum(int(dsum[i].decisions == d) for i, d in zip(idx, rdec)),
+                "per_policy": {p: sum(int(x == p) for x in pol) for p in sorted(set(pol))}}
+        if not args.no_configs:
+            try:
+                line["configs"] = baseline_configs_line(torch, local)
+            except Exception as exc:  # noqa: BLE001 — keep the headline line
+                line["configs"] = {"error": repr(exc)}
         print(json.dumps(line), flush=True)
     batch.close()
     if world > 1:

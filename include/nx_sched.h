@@ -305,7 +305,19 @@ typedef struct nx_request_record { /* servesim::RequestRecord, metrics.h:12-20 *
  * SoA image into pinned host memory. No device work. */
 int nx_sim_create_json(const char* const* configs, int32_t n_replicas, int32_t device,
                        int32_t host_threads, nx_sim_t* out);
-/* Upload (H2D), launch, download (D2H) on the handle's stream; each is async. */
+/* A failed replica's status (NX_OK when it ran to completion) and the
+ * reference's exception text for it (e.g. engine.cpp:75-78 "prefill_priority:
+ * prompt exceeds m_max; raise m_max for engine 3") into buf[cap]. Valid after
+ * the download. */
+int nx_sim_error(nx_sim_t h, int32_t replica, char* buf, int64_t cap);
+/* Workload generation again (build_workload, proj/src/sim.cpp:101-141) for
+ * every replica on host threads, into the pinned input image; the parsed
+ * configs are kept. Deterministic: the next run reproduces the same results.
+ * (bench.py times it inside e2e, as the reference's run_simulation clock
+ * includes its workload build.) */
+int nx_sim_rebuild_workloads(nx_sim_t h, int32_t host_threads);
+/* Upload (H2D), launch, download (D2H) on the handle's stream; each is async.
+ * nx_sim_last_kernel_ms covers the launch's state reset + the kernel. */
 int nx_sim_upload(nx_sim_t h);
 int nx_sim_launch(nx_sim_t h);
 int nx_sim_download(nx_sim_t h);

@@ -76,6 +76,8 @@ def lib() -> C.CDLL:
     L.nx_sim_last_kernel_ms.argtypes = [C.c_void_p, _P(C.c_float)]
     L.nx_sim_io_bytes.argtypes = [C.c_void_p, _P(C.c_int64), _P(C.c_int64)]
     L.nx_sim_summaries.argtypes = [C.c_void_p, _P(ReplicaSummary)]
+    L.nx_sim_error.argtypes = [C.c_void_p, C.c_int32, C.c_char_p, C.c_int64]
+    L.nx_sim_rebuild_workloads.argtypes = [C.c_void_p, C.c_int32]
     L.nx_sim_summary_json.argtypes = [C.c_void_p, C.c_int32, C.c_char_p, C.c_int64, _P(C.c_int64)]
     L.nx_sim_records.argtypes = [C.c_void_p, C.c_int32, _P(RequestRecord), C.c_int64, _P(C.c_int64)]
     L.nx_sim_learner.argtypes = [C.c_void_p, C.c_int32, C.c_int32, _P(C.c_double), _P(C.c_int64),

@@ -1209,8 +1209,13 @@ nx_sim_kernel(const NxPools* __restrict__ pools, const int32_t* __restrict__ ord
       if (s_excl) {
         const int e = atomicAdd(&ctl[1], 1);
         if (e < n_excl) slot = e;
+        // the exclusive replicas were already taken (a late-starting CTA:
+        // others drained them): release the waiting sibling now, since the
+        // release after a completed exclusive replica will not happen
+        else atomicExch(&sm_state[smid], 3);
         s_excl = 0;  // one exclusive replica, then release the sibling
-      } else {
+      }
+      if (slot == n_rep) {
         const int k = n_excl + atomicAdd(&ctl[0], 1);
         if (k < n_rep) {
           slot = k;

@@ -501,6 +501,58 @@ const char* site_name(int site) {
   return "error";
 }
 
+// The reference's exception text for a failed replica (the throw sites are
+// cited in nx_layout.h NX_SITE_*); err_info carries the engine id where the
+// reference message names one (engine.cpp:75-78).
+std::string replica_message(const NxReplicaOut& o) {
+  if (o.err_site == NX_SITE_PREFILL_CAP)
+    return "prefill_priority: prompt exceeds m_max; raise m_max for engine " + std::to_string(o.err_info);
+  return site_name(o.err_site);
+}
+
+// Device-path limits the reference does not have: the engine and learner
+// knobs travel as int32 in NxEngineDesc / NxReplicaDesc (nx_layout.h), and a
+// replica CTA stages q_max + 1 prefix sums per warp in shared memory. Values
+// the reference would accept but the device cannot represent are rejected
+// here with std::invalid_argument instead of being narrowed silently.
+void check_device_limits(const nx::RunCfg& c, size_t smem_optin) {
+  auto i32 = [](int64_t v, const std::string& what) {
+    if (v < INT32_MIN || v > INT32_MAX)
+      throw std::invalid_argument(what + " = " + std::to_string(v) +
+                                  ": the device path supports 32-bit values");
+  };
+  i32(c.long_window, "learner.long_window");
+  i32(c.short_window, "learner.short_window");
+  i32(c.structural_period, "learner.structural_period");
+  i32(c.linear_period, "learner.linear_period");
+  for (const auto& e : c.engines) {
+    const std::string id = "engine " + std::to_string(e.engine_id) + ": ";
+    i32(e.kv_blocks, id + "kv_blocks");
+    i32(e.block_size, id + "block_size");
+    i32(e.m_max, id + "m_max");
+    i32(e.q_max, id + "q_max");
+    i32(e.static_budget, id + "static_budget");
+    i32(e.wait_cap, id + "wait_cap");
+    // KV reservations and token counts are int32 sums of blocks
+    if (e.kv_blocks > 0 && e.block_size > 0 && e.kv_blocks > INT32_MAX / 2)
+      throw std::invalid_argument(id + "kv_blocks = " + std::to_string(e.kv_blocks) +
+                                  ": the device path supports kv_blocks <= 2^30");
+    if (smem_optin > 0) {
+      const size_t need = nx_sim_smem_per_warp(static_cast<int>(c.engines.size()),
+                                               static_cast<int>(e.q_max) + 1);
+      if (need > smem_optin) {
+        int64_t lim = e.q_max;
+        while (lim > 1 && nx_sim_smem_per_warp(static_cast<int>(c.engines.size()),
+                                               static_cast<int>(lim) + 1) > smem_optin)
+          lim = lim * 7 / 8;
+        throw std::invalid_argument(id + "q_max = " + std::to_string(e.q_max) +
+                                    ": the device path supports q_max <= " + std::to_string(lim) +
+                                    " with " + std::to_string(c.engines.size()) + " engines");
+      }
+    }
+  }
+}
+
 }  // namespace
 
 extern "C" {
@@ -523,6 +575,16 @@ int nx_sim_create_json(const char* const* configs, int32_t n_replicas, int32_t d
     h->n_rep = n_replicas;
     h->cfgs.resize(n_replicas);
     h->wl.resize(n_replicas);
+    // shared-memory limit of the replica CTA (0 when no device is visible:
+    // the check then happens at launch)
+    size_t smem_optin = 0;
+    {
+      int v = 0;
+      if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, device) == cudaSuccess && v > 0)
+        smem_optin = static_cast<size_t>(v);
+      else
+        cudaGetLastError();
+    }
     // parse + synthesise on host threads (reference semantics, host libm)
     std::atomic<int> next{0};
     std::vector<std::string> errs(n_replicas);
@@ -533,6 +595,7 @@ int nx_sim_create_json(const char* const* configs, int32_t n_replicas, int32_t d
           h->cfgs[i] = nx::parse_run_config(configs[i]);
           if (h->cfgs[i].engines.size() > NX_MAX_ENGINES)
             throw std::invalid_argument("device path supports at most 32 engines per replica");
+          check_device_limits(h->cfgs[i], smem_optin);
           h->wl[i] = nx::build_workload(h->cfgs[i]);
           if (h->wl[i].prompt.size() > (1u << 30))
             throw std::invalid_argument("too many requests for one replica");
@@ -553,6 +616,44 @@ int nx_sim_create_json(const char* const* configs, int32_t n_replicas, int32_t d
     cuda_check(cudaEventCreate(&h->ev1), "cudaEventCreate");
     fill_descriptors(*h);
     *out = h.release();
+  });
+}
+
+int nx_sim_rebuild_workloads(nx_sim_t h, int32_t host_threads) {
+  return guard([&] {
+    // build_workload (sim.cpp:101-141) again for every replica on host
+    // threads, then the pinned input image; configs stay parsed (the
+    // reference's own clock also starts after RunConfig parsing)
+    std::atomic<int> next{0};
+    std::vector<std::string> errs(h->n_rep);
+    std::vector<int> codes(h->n_rep, 0);
+    auto work = [&] {
+      for (int i = next++; i < h->n_rep; i = next++) {
+        codes[i] = guard([&] {
+          nx::Workload w = nx::build_workload(h->cfgs[i]);
+          if (w.prompt.size() != h->wl[i].prompt.size() || w.session_names.size() != h->wl[i].session_names.size())
+            throw std::logic_error("nx_sim_rebuild_workloads: workload shape changed");
+          h->wl[i] = std::move(w);
+        });
+        if (codes[i]) errs[i] = g_err;
+      }
+    };
+    const int nt = std::max(1, std::min<int>(host_threads > 0 ? host_threads : 1, h->n_rep));
+    std::vector<std::thread> pool;
+    for (int t = 1; t < nt; ++t) pool.emplace_back(work);
+    work();
+    for (auto& t : pool) t.join();
+    for (int i = 0; i < h->n_rep; ++i)
+      if (codes[i]) throw NxError(codes[i], "replica " + std::to_string(i) + ": " + errs[i]);
+    for (int r = 0; r < h->n_rep; ++r) {
+      const nx::Workload& w = h->wl[r];
+      const int64_t o = h->rep[r].req_off;
+      const size_t n = w.prompt.size();
+      std::memcpy(h->h_arr_us + o, w.arrival_us.data(), n * sizeof(int64_t));
+      std::memcpy(h->h_arr_ms + o, w.arrival_ms.data(), n * sizeof(double));
+      for (size_t i = 0; i < n; ++i) h->h_req0[o + i] = {0, 0, w.prompt[i], w.output[i]};
+      std::memcpy(h->h_session + o, w.session.data(), n * sizeof(int32_t));
+    }
   });
 }
 
@@ -579,6 +680,8 @@ int nx_sim_launch(nx_sim_t h) {
   return guard([&] {
     cuda_check(cudaSetDevice(h->device), "cudaSetDevice");
     cudaStream_t st = h->stream;
+    // the launch's device time covers the per-launch state reset too
+    cuda_check(cudaEventRecord(h->ev0, st), "event");
     cuda_check(cudaMemsetAsync(h->d_arena + h->off_state_begin, 0,
                                h->off_state_end - h->off_state_begin, st), "memset state");
     cuda_check(cudaMemsetAsync(h->d_arena + h->off_ff_begin, 0xff,
@@ -600,7 +703,6 @@ int nx_sim_launch(nx_sim_t h) {
     per_sm = std::min(per_sm, cap_sm);
     const int need = h->n_rep;
     const int grid = std::max(1, std::min(need, per_sm * sm_count(h->device)));
-    cuda_check(cudaEventRecord(h->ev0, st), "event");
     // exclusive SMs: the replicas within 10% of the longest expected cost,
     // when the batch is skewed (longest > 1.5x mean) and fills 2 CTAs on
     // every SM; at most a quarter of the SMs
@@ -699,6 +801,21 @@ int nx_sim_summaries(nx_sim_t h, nx_replica_summary* out) {
   });
 }
 
+int nx_sim_error(nx_sim_t h, int32_t replica, char* buf, int64_t cap) {
+  if (!h || replica < 0 || replica >= h->n_rep) {
+    g_err = "nx_sim_error: replica out of range";
+    return NX_EINVAL;
+  }
+  const NxReplicaOut& o = h->h_rep_out[replica];
+  const std::string msg = o.status ? replica_message(o) : std::string();
+  if (buf && cap > 0) {
+    const size_t k = std::min<size_t>(msg.size(), static_cast<size_t>(cap - 1));
+    std::memcpy(buf, msg.data(), k);
+    buf[k] = 0;
+  }
+  return o.status;
+}
+
 int nx_sim_records(nx_sim_t h, int32_t replica, nx_request_record* out, int64_t cap, int64_t* n) {
   return guard([&] {
     if (replica < 0 || replica >= h->n_rep) throw std::invalid_argument("replica out of range");
@@ -727,7 +844,7 @@ int nx_sim_summary_json(nx_sim_t h, int32_t replica, char* buf, int64_t cap, int
     if (replica < 0 || replica >= h->n_rep) throw std::invalid_argument("replica out of range");
     const NxReplicaOut& o = h->h_rep_out[replica];
     if (o.status != 0) {
-      const std::string msg = site_name(o.err_site);
+      const std::string msg = replica_message(o);
       if (o.status == 1) throw std::invalid_argument(msg);
       if (o.status == 3) throw std::logic_error(msg);
       throw std::runtime_error(msg);

@@ -1084,8 +1084,10 @@ void RunConfig::validate() const {
 }
 
 namespace {
-void raise_replica(const nx_replica_summary& s) {
-  std::string msg = nx_last_error();
+void raise_replica(nx_sim_t h, int32_t r, const nx_replica_summary& s) {
+  char buf[512];
+  nx_sim_error(h, r, buf, sizeof buf);
+  std::string msg = buf;
   if (msg.empty()) msg = "device replica failed";
   if (s.status == NX_EINVAL) throw std::invalid_argument(msg);
   if (s.status == NX_ELOGIC) throw std::logic_error(msg);
@@ -1141,7 +1143,7 @@ std::vector<RunResult> run_replicas(std::span<const RunConfig> cfgs, int device)
   raise(nx_sim_summaries(S.h, sums.data()));
   std::vector<RunResult> out;
   for (size_t r = 0; r < cfgs.size(); ++r) {
-    if (sums[r].status != NX_OK) raise_replica(sums[r]);
+    if (sums[r].status != NX_OK) raise_replica(S.h, static_cast<int32_t>(r), sums[r]);
     const RunConfig& c = cfgs[r];
     RunResult res = result_of(S.h, static_cast<int32_t>(r), sums[r]);
     res.metrics = summarize(res.records, c.slo);
@@ -1200,6 +1202,25 @@ SweepResult sweep(const RunConfig& base, SweepAxis axis, const std::vector<std::
     }
     out.rows.push_back(std::move(row));
   }
+  // a workload that fails to build (e.g. an unreadable trace) fails only its
+  // own row, like the reference's per-value try/catch (sim.cpp:608-642)
+  {
+    std::vector<RunConfig> keep;
+    std::vector<size_t> keep_row;
+    for (size_t k = 0; k < cfgs.size(); ++k) {
+      const std::string t = cfgs[k].to_json_text();
+      uint64_t ah = 0;
+      int64_t nr = 0, ns = 0;
+      if (nx_workload_info(t.c_str(), &ah, &nr, &ns) != NX_OK) {
+        out.rows[row_of_cfg[k]].error = nx_last_error();
+        continue;
+      }
+      keep.push_back(cfgs[k]);
+      keep_row.push_back(row_of_cfg[k]);
+    }
+    cfgs = std::move(keep);
+    row_of_cfg = std::move(keep_row);
+  }
   if (cfgs.empty()) return out;
   std::vector<std::string> texts;
   std::vector<const char*> ptrs;
@@ -1218,7 +1239,7 @@ SweepResult sweep(const RunConfig& base, SweepAxis axis, const std::vector<std::
   for (size_t k = 0; k < cfgs.size(); ++k) {
     SweepRow& row = out.rows[row_of_cfg[k]];
     try {
-      if (sums[k].status != NX_OK) raise_replica(sums[k]);
+      if (sums[k].status != NX_OK) raise_replica(S.h, static_cast<int32_t>(k), sums[k]);
       row.result = result_of(S.h, static_cast<int32_t>(k), sums[k]);
       row.result.metrics = summarize(row.result.records, cfgs[k].slo);
       row.ok = true;

@@ -55,6 +55,10 @@ class Batch:
         self.h = h
         self.n = len(texts)
 
+    def rebuild_workloads(self, host_threads: int | None = None):
+        """Regenerate every replica's workload on the host (same results)."""
+        check(lib().nx_sim_rebuild_workloads(self.h, host_threads or max(1, os.cpu_count() or 1)))
+
     def upload(self):
         check(lib().nx_sim_upload(self.h))
 
@@ -166,10 +170,16 @@ class Batch:
         """Simulation::write_outputs (sim.cpp:393-413) into the config's output.dir."""
         check(lib().nx_sim_write_outputs(self.h, r))
 
+    def error(self, r: int) -> str:
+        """The reference's exception text for a failed replica ('' if it ran)."""
+        buf = C.create_string_buffer(512)
+        lib().nx_sim_error(self.h, r, buf, 512)
+        return buf.value.decode()
+
     def result(self, r: int, with_records: bool = True, n_engines: int | None = None) -> RunResult:
         s = self.summaries()[r]
         if s.status != 0:
-            _raise_status(s)
+            _raise_status(s, self.error(r))
         sj = self.summary_json(r)
         ne = n_engines if n_engines is not None else len(json.loads(sj)["learners"])
         return RunResult(s.arrived, s.completed, s.rejected, s.unfinished, s.arrival_hash,
@@ -189,8 +199,8 @@ class Batch:
             pass
 
 
-def _raise_status(s):
-    msg = f"device replica failed at site {s.err_site}"
+def _raise_status(s, msg: str = ""):
+    msg = msg or f"device replica failed at site {s.err_site}"
     if s.status == _lib.NX_EINVAL:
         raise ValueError(msg)
     if s.status == _lib.NX_ELOGIC:
@@ -225,29 +235,37 @@ def sweep(base: dict, axis: str, values, device: int = 0):
     reported per row, like the reference."""
     if axis not in ("rate", "policy", "budget"):
         raise RuntimeError(f"unknown sweep axis: {axis}")
-    cfgs = []
-    for v in values:
-        c = copy.deepcopy(base)
-        c.setdefault("output", {})["dir"] = ""
-        if axis == "rate":
-            c.setdefault("workload", {})["mode"] = "qps"
-            c["workload"]["rate"] = float(v)
-        elif axis == "policy":
-            for e in c["engines"]:
-                e["scheduler_policy"] = v
-        else:
-            for e in c["engines"]:
-                e["static_budget"] = int(v)
+    rows = [{"value": str(v), "ok": False, "error": ""} for v in values]
+    cfgs, where = [], []
+    for i, v in enumerate(values):
+        try:
+            c = copy.deepcopy(base)
+            c.setdefault("output", {})["dir"] = ""
+            if axis == "rate":
+                c.setdefault("workload", {})["mode"] = "qps"
+                c["workload"]["rate"] = float(v)
+            elif axis == "policy":
+                for e in c["engines"]:
+                    e["scheduler_policy"] = v
+            else:
+                for e in c["engines"]:
+                    e["static_budget"] = int(v)
+            workload_info(c)  # parse + validate + build the workload (host only)
+        except Exception as exc:  # noqa: BLE001 — the row records it (sim.cpp:608-642)
+            rows[i]["error"] = str(exc)
+            continue
         cfgs.append(c)
-    rows = []
+        where.append(i)
+    if not cfgs:
+        return {"axis": axis, "rows": rows}
     b = Batch(cfgs, device).run()
     try:
         sums = b.summaries()
-        for i, v in enumerate(values):
-            if sums[i].status != 0:
-                rows.append({"value": str(v), "ok": False, "error": f"site {sums[i].err_site}"})
+        for k, i in enumerate(where):
+            if sums[k].status != 0:
+                rows[i]["error"] = b.error(k)
             else:
-                rows.append({"value": str(v), "ok": True, "result": b.result(i, False)})
+                rows[i] = {"value": rows[i]["value"], "ok": True, "result": b.result(k, False)}
     finally:
         b.close()
     return {"axis": axis, "rows": rows}

@@ -110,6 +110,28 @@ def config4(trace_path: str, seed: int = 4) -> dict:
     }
 
 
+def baseline_configs(tmpdir, synth) -> dict:
+    """BASELINE.json configs 1-4 at their stated sizes:
+    1k-request single-engine LENS; 10k-request Gamma CV 3 traces at 20 and
+    40 req/s over 4 PRISM engines; 100k requests over 8 heterogeneous
+    engines; 2k long-context prompts (8k-128k tokens) over 4 engines with
+    65,536 KV blocks. Traces are written under `tmpdir` with `synth` (the
+    host synthesiser, reference synth_generate semantics)."""
+    g20 = os.path.join(str(tmpdir), "gamma_cv3_r20.jsonl")
+    g40 = os.path.join(str(tmpdir), "gamma_cv3_r40.jsonl")
+    lc = os.path.join(str(tmpdir), "longctx_2k.jsonl")
+    write_gamma_trace(g20, synth, n=10_000, rate=20.0, seed=2)
+    write_gamma_trace(g40, synth, n=10_000, rate=40.0, seed=2)
+    write_longctx_trace(lc, synth, n=2000, rate=0.5, seed=4)
+    return {
+        "config1_lens_1k": config1(),
+        "config2_gamma_r20_10k": config2(g20, rate=20.0),
+        "config2_gamma_r40_10k": config2(g40, rate=40.0),
+        "config3_het8_100k": config3(),
+        "config4_longctx_2k": config4(lc),
+    }
+
+
 def write_jsonl_trace(path: str | os.PathLike, arrivals, prompts, outputs, sessions) -> None:
     """Reference trace format (workload.cpp:123-135). Python's json emits the
     shortest round-trip repr for floats, so every reader parses the same doubles."""

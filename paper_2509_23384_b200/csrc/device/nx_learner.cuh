@@ -970,7 +970,7 @@ static __device__ double exact_elem(Ctx& c, Stage& S, double kB, double kS);
 static __device__ FitOut gauged_fit(Ctx& c, Stage& S, const Params& cur, double kB, double kS, bool exact = false) {
   const long long t0 = nx_clock();
   FitOut o = gauged_fit_impl(c, S, cur, kB, kS, exact);
-  if (c.lane == 0) count(c.rs->cycles[10], nx_clock() - t0);
+  if (c.lane == 0) count(c.rs->lcycles[10], nx_clock() - t0);
   return o;
 }
 static __device__ NX_COLD FitOut gauged_fit_impl(Ctx& c, Stage& S, const Params& cur, double kB, double kS,
@@ -1016,7 +1016,7 @@ static __device__ NX_COLD FitOut gauged_fit_impl(Ctx& c, Stage& S, const Params&
     __syncwarp();
   }
   const long long tf1 = nx_clock();
-  if (c.lane == 0) count(c.rs->cycles[7], tf1 - tf0);
+  if (c.lane == 0) count(c.rs->lcycles[7], tf1 - tf0);
   // per-entry totals (fixed combination order across the team; every term is
   // positive, so the closed-form SSE bound covers any order)
   double tot[11];
@@ -1068,7 +1068,7 @@ static __device__ NX_COLD FitOut gauged_fit_impl(Ctx& c, Stage& S, const Params&
       else sum_over_s(t, c.lane, 32, a);
       warp_sum11(a, tot);
     }
-    if (c.lane == 0 && op != 1) count(c.rs->cycles[11], nx_clock() - tq);
+    if (c.lane == 0 && op != 1) count(c.rs->lcycles[11], nx_clock() - tq);
 #ifdef NX_TRACE_FIT
     if (op != 1 && S.n == 1024) {
       if (kS != S.ifs_k) {
@@ -1116,7 +1116,7 @@ static __device__ NX_COLD FitOut gauged_fit_impl(Ctx& c, Stage& S, const Params&
     tot[8] = warp_sum(a24); tot[9] = warp_sum(t1); tot[10] = warp_sum(t2);
   }
   if (need_fs) S.ifs_k = kS;
-  if (c.lane == 0) count(c.rs->cycles[9], nx_clock() - tf1);
+  if (c.lane == 0) count(c.rs->lcycles[9], nx_clock() - tf1);
   const long long tf2 = nx_clock();
   const double u15[15] = {S.A00, tot[0], tot[1], S.A03, S.A04, tot[2], tot[3], tot[5], tot[6],
                           tot[4], tot[7], tot[8], S.A33, S.A34, S.A44};
@@ -1135,7 +1135,7 @@ static __device__ NX_COLD FitOut gauged_fit_impl(Ctx& c, Stage& S, const Params&
     if (pass > 0 || !ambiguous) break;
     e = exact_elem(c, S, kB, kS);
   }
-  if (c.lane == 0) count(c.rs->cycles[13], nx_clock() - ts);
+  if (c.lane == 0) count(c.rs->lcycles[13], nx_clock() - ts);
   return out;
 }
 
@@ -1219,7 +1219,7 @@ static __device__ NX_COLD FitOut finish_fit(Ctx& c, const Stage& S, const Params
   bool okk[2], amb[2];
   const long long ts5 = nx_clock();
   solve5_warp_k<2>(vk, xk, okk, amb);
-  if (c.lane == 0) count(c.rs->cycles[15], nx_clock() - ts5);
+  if (c.lane == 0) count(c.rs->lcycles[15], nx_clock() - ts5);
   if (ambiguous && amb[0]) *ambiguous = true;
   if (!okk[0]) return out;
 #pragma unroll
@@ -1316,7 +1316,7 @@ static __device__ NX_COLD void update_structural(Ctx& c, int e) {
   int shaped, bmax;
   const long long ts0 = nx_clock();
   stage_window(c, w, cur, S, saturated, shaped, bmax);
-  if (c.lane == 0) count(c.rs->cycles[12], nx_clock() - ts0);
+  if (c.lane == 0) count(c.rs->lcycles[12], nx_clock() - ts0);
   if (saturated || shaped < 16) {
     __syncwarp();
     if (c.lane == 0) g.cnt[6] += 1;
@@ -1397,7 +1397,7 @@ static __device__ NX_COLD void update_structural(Ctx& c, int e) {
   {
     const long long tx = nx_clock();
     const FitOut ex = gauged_fit(c, S, cur, best.p.kB, best.p.kS, true);
-    if (c.lane == 0) count(c.rs->cycles[14], nx_clock() - tx);
+    if (c.lane == 0) count(c.rs->lcycles[14], nx_clock() - tx);
     if (isfinite(ex.err)) best = ex;
     else best.err = ex.err;  // the exact system is singular: the reference fails this fit too
   }
@@ -1463,7 +1463,7 @@ static __device__ void wait_refit(Ctx& c, int e) {
   }
   __threadfence_block();
   __syncwarp();
-  if (c.lane == 0) count(c.rs->cycles[8], nx_clock() - t0);
+  if (c.lane == 0) count(c.rs->lcycles[8], nx_clock() - t0);
 }
 
 // The refit leader (warp 1): claims the next job (engine id) and runs
@@ -1541,7 +1541,16 @@ static __device__ NX_COLD void record_sample(Ctx& c, int e, int b, int s, double
     PhaseTimer pt(c.rs, 5);
     update_linear(c, e);
   }
-  if (seen >= c.d->min_s && g.str_left == c.d->s_period) post_refit(c, e);
+  if (seen >= c.d->min_s && g.str_left == c.d->s_period) {
+    // engine-parallel loop: the engine's own warp refits (its timeline waits
+    // for the new params anyway; other engines' warps keep running)
+#ifdef NX_INLINE_REFIT
+    PhaseTimer pt(c.rs, 6);
+    update_structural(c, e);
+#else
+    post_refit(c, e);
+#endif
+  }
 }
 
 }  // namespace nxd

@@ -77,7 +77,15 @@ struct EngSm {
   int64_t started_us, seen, rep_qlen, tw_degen;
   int32_t lin_left, str_left;                  // samples until the next linear / structural period
   int64_t cnt[7];                              // LearnerCounters
+  // parent references of the pending events (sim_kernel.cu: log index of the
+  // event that pushed them, kRootPar | seq of a root parent, kSelfRoot | seq
+  // for the initial state reports)
   uint32_t step_seq, learn_seq, report_seq, dq_s0;
+  uint32_t log_n;                              // events this engine has logged
+  uint32_t last_fin_par;                       // key of the last step that completed requests
+  uint64_t last_fin_t;                         // (kNoEvent: none)
+  int64_t period_us;                           // state_report_period (shared-memory copy)
+  int32_t eid1;                                // engine_id + 1 (event hash)
   int32_t wq_head, wq_len, rq_len;
   int32_t pinned, reserved, cache_blocks, lru_head, lru_tail;
   int32_t busy, plan_n, plan_b, plan_s, plan_wspan, plan_overload, plan_ndec;
@@ -91,12 +99,23 @@ struct EngSm {
   double memo_pred, memo_truth;
 };
 
+struct ErrSlot {                               // first error raised by one warp
+  int32_t status, site;
+  int64_t info;
+  uint64_t t;                                  // key of the event that raised it
+  uint32_t par;
+  int32_t kind, eng;
+};
+
+constexpr int kPdMaxWarps = 9;                 // router + up to 8 engine warps per replica CTA
+
 struct RepSm {
   uint64_t ev_hash, rr_next, rng[4];
   uint64_t next_arr;                           // arrival time at the cursor (cached)
   int64_t arrived, rejected, pending, n_rec, events, info;
   int64_t work[6];
   int64_t cycles[16];
+  int64_t lcycles[16];                         // learner-internal timers (diagnostic build)
   int64_t t_begin_ns;
   int64_t n_plan_log, n_route_log, n_learn_log;
   double l_bar_ema;
@@ -106,6 +125,22 @@ struct RepSm {
   int32_t jq_eng[64];
   TeamTask team;                               // refit leader -> helpers
   double team_part[kRefitWarps][11];           // per-warp fit-pass totals
+  // engine-parallel event loop (sim_kernel.cu)
+  ErrSlot err[kPdMaxWarps];
+  uint64_t horizon;                            // engines process events with key < (horizon, arrival)
+  uint64_t front[NX_MAX_ENGINES];              // next event time of each engine
+  uint64_t kd_t;                               // drain key: last completion / last arrival
+  uint32_t kd_par;
+  int32_t kd_kind, kd_eng, kd_ready, kd_inf;
+  int32_t final_mode, stop, parked, n_done, n_fin;
+  int32_t all_arrived;
+  uint32_t wpos[NX_MAX_ENGINES], mpos[NX_MAX_ENGINES];  // log entries written / merged
+  int32_t ob_w[NX_MAX_ENGINES], ob_r[NX_MAX_ENGINES];   // outbox written / merged
+  int32_t ps_w[NX_MAX_ENGINES], ps_r[NX_MAX_ENGINES];   // staged plan rows
+  int32_t ls_w[NX_MAX_ENGINES], ls_r[NX_MAX_ENGINES];   // staged learner rows
+  int32_t done[NX_MAX_ENGINES], fin[NX_MAX_ENGINES];
+  int32_t am;                                  // arrivals merged
+  uint64_t am_t;                               // time of the next routed, unmerged arrival
 };
 
 struct Ctx {
@@ -125,6 +160,15 @@ struct Ctx {
   int team;                // warps in the refit team (1: the calling warp alone)
   double* fsm;             // shared-memory fit tables (1/f_B, then 1/f_S); nullptr: use scratch
   int fsm_cap;             // 1/f_S entries that fit in fsm
+  ErrSlot* err;            // this warp's error slot
+  uint32_t cur_ref;        // parent reference for events pushed by the current handler
+  uint32_t cur_meta;       // log flags gathered while handling the current event
+  int began;               // try_begin_step started a step and staged a plan row
+  int inline_refit;        // structural refits run on the calling warp (no refit team)
+  NxEvLog* elog;           // this CTA slot's event-log rings (engine e at e * evlog_cap)
+  int32_t* obox;           // this CTA slot's outboxes
+  int64_t ob_cap;          // outbox entries per engine
+  NxEvLog* sring;          // shared-memory copies of the rings' most recent entries
 };
 
 template <class T>
@@ -137,14 +181,16 @@ __device__ __forceinline__ void put(T& dst, T v) {
 // Raise a reference exception: first error wins, replica stops.
 __device__ __forceinline__ void fail(Ctx& c, int status, int site, int64_t info) {
   __syncwarp();
-  if (c.lane == 0 && c.rs->status == 0) {
-    c.rs->status = status;
-    c.rs->site = site;
-    c.rs->info = info;
+  if (c.lane == 0 && c.err->status == 0) {
+    c.err->status = status;
+    c.err->site = site;
+    c.err->info = info;
   }
   __syncwarp();
 }
-__device__ __forceinline__ bool failed(const Ctx& c) { return c.rs->status != 0; }
+__device__ __forceinline__ bool failed(const Ctx& c) {
+  return *reinterpret_cast<const volatile int32_t*>(&c.err->status) != 0;
+}
 
 // Phase timers exist only in the diagnostic build (-DNX_TIMERS, made by
 // tools/phase_report.py); the product kernel compiles every clock read and

@@ -336,7 +336,7 @@ __global__ void __launch_bounds__(32) nx_refit_kernel(int kind, const nx_refit_p
         sm.ed.ring_off = pr.sample_off + (n - keep);
         for (int i = 0; i < 6; ++i) sm.rs.work[i] = 0;
         for (int i = 0; i < 16; ++i) sm.rs.cycles[i] = 0;
-        sm.rs.status = 0;
+        sm.rs.err[0].status = 0;
         sm.eng.lp = prior;
         sm.eng.ring_size = keep;
         sm.eng.ring_head = 0;
@@ -349,6 +349,8 @@ __global__ void __launch_bounds__(32) nx_refit_kernel(int kind, const nx_refit_p
       c.d = &sm.rep;
       c.ed = &sm.ed;
       c.rs = &sm.rs;
+      c.err = &sm.rs.err[0];
+      c.inline_refit = 1;
       c.eng = &sm.eng;
       c.chunk = sm.chunk;
       c.prefix = reinterpret_cast<int32_t*>(sm.chunk);

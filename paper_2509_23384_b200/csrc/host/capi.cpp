@@ -29,8 +29,40 @@
 #include "report.hpp"
 
 extern "C" cudaError_t nx_launch_sim(const NxPools* d_pools, const int32_t* d_order, int n_rep,
-                                     int* d_next, int smem_per_warp, int prefix_cap, int max_eng,
-                                     int grid, int warps_per_block, int n_excl, cudaStream_t st);
+                                     int* d_next, int prefix_cap, int max_eng, int n_ew, int fsm_cap,
+                                     size_t smem, int grid, cudaStream_t st);
+extern "C" size_t nx_sim_fit_table_doubles(int fsm_cap);
+extern "C" cudaError_t nx_sim_set_debug(unsigned long long* dev_ptr);
+
+namespace {
+// NX_DEBUG=1: the simulation kernel's spin-wait watchdog dumps its replica
+// CTA's event-loop state into host-mapped memory before it traps.
+unsigned long long* g_dbg_host = nullptr;
+void arm_debug_dump() {
+  const char* v = std::getenv("NX_DEBUG");
+  if (!v || v[0] != '1' || g_dbg_host) return;
+  void* p = nullptr;
+  if (cudaHostAlloc(&p, 4096, cudaHostAllocMapped) != cudaSuccess) return;
+  std::memset(p, 0, 4096);
+  void* dp = nullptr;
+  cudaHostGetDevicePointer(&dp, p, 0);
+  g_dbg_host = static_cast<unsigned long long*>(p);
+  nx_sim_set_debug(static_cast<unsigned long long*>(dp));
+}
+void print_debug_dump() {
+  if (!g_dbg_host || g_dbg_host[0] == 0) return;
+  const unsigned long long* d = g_dbg_host;
+  std::fprintf(stderr, "[nx debug] line %llu warp %llu block %llu horizon %llu next_arr %llu final %llu parked %llu "
+               "n_done %llu n_fin %llu kd_ready %llu cursor %llu am %llu n_eng %llu stop %llu kd_inf %llu\n",
+               d[1], d[2], d[3], d[4], d[5], d[6], d[7], d[8], d[9], d[10], d[11], d[12], d[13], d[14], d[15]);
+  for (unsigned long long e = 0; e < d[13] && e < 8; ++e) {
+    const unsigned long long* q = d + 16 + 10 * e;
+    std::fprintf(stderr, "[nx debug] eng %llu front %llu wpos %llu mpos %llu step %llu report %llu learn %llu dq %llu "
+                 "flags %llx log_n %llu wq %llu rq %llu\n",
+                 e, q[0], q[1], q[2], q[3], q[4], q[5], q[6], q[7], q[8], q[9] & 0xffffffffull, q[9] >> 32);
+  }
+}
+}  // namespace
 extern "C" cudaError_t nx_sim_occupancy(int warps_per_block, size_t smem, int* blocks_per_sm);
 extern "C" size_t nx_sim_smem_per_warp(int max_engines, int prefix_cap);
 extern "C" cudaError_t nx_launch_perf_eval(const double* params, int n_params, const int32_t* idx,
@@ -105,10 +137,12 @@ struct Arena {
   }
 };
 
-#ifndef NX_REFIT_WARPS
-#define NX_REFIT_WARPS 3
-#endif
-constexpr int kWarpsPerBlock = 1 + NX_REFIT_WARPS;  // event-loop warp + refit warps per replica CTA
+// Replica CTA: a router warp + one warp per engine (engines beyond
+// kEngineWarps share warps round-robin); sim_kernel.cu kPdMaxWarps.
+constexpr int kEngineWarps = 8;
+// Event-log ring entries per engine (power of two): the merger's and the key
+// comparisons' window into an engine's past events.
+constexpr int64_t kEvLogCap = NX_EVLOG_CAP;
 
 
 // Stream-ordered scratch (cudaMallocAsync) for the batched operators: keep
@@ -178,6 +212,9 @@ struct nx_sim {
   std::vector<nx::RunCfg> cfgs;
   std::vector<nx::Workload> wl;
   int n_rep = 0, max_eng = 1, prefix_cap = 1;
+  int n_ew = 1, slots = 1;                 // engine warps per CTA, CTA slots (resident replicas)
+  int per_sm = 1;                          // resident replica CTAs per SM
+  int64_t max_req = 1, max_long = 1;
   int64_t n_req = 0, n_sess = 0, n_eng = 0;
   // host pinned input image
   std::vector<NxReplicaDesc> rep;
@@ -301,9 +338,8 @@ void fill_descriptors(nx_sim& h) {
     h.n_learn_log += d.learn_log_cap;
     req_off += n;
     sess_off += ns;
-    // learner scratch for the event-loop warp and the refit leader
-    // (nx_state.cuh refit_scratch_stride)
-    scratch_off += 2 * nx_refit_scratch_per(static_cast<int64_t>(c.long_window));
+    h.max_req = std::max<int64_t>(h.max_req, n);
+    h.max_long = std::max<int64_t>(h.max_long, c.long_window);
     for (const auto& ec : c.engines) {
       NxEngineDesc e;
       std::memset(&e, 0, sizeof e);
@@ -354,6 +390,26 @@ void fill_descriptors(nx_sim& h) {
   h.n_req = req_off;
   h.n_sess = sess_off;
   h.n_eng = static_cast<int64_t>(h.eng.size());
+  // per CTA slot (one resident replica per SM): event-log rings, outboxes and
+  // learner scratch for every engine warp
+  int ew = kEngineWarps;
+  if (const char* v = std::getenv("NX_ENGINE_WARPS")) ew = std::max(1, std::min(kEngineWarps, std::atoi(v)));
+  h.n_ew = std::min(ew, h.max_eng);
+  // resident CTAs per SM: the register file bounds it (occupancy query with
+  // the base shared memory; the fit tables then share what is left)
+  {
+    const size_t base = nx_sim_smem_per_warp(h.max_eng, h.prefix_cap);
+    int occ = 0;
+    cuda_check(nx_sim_occupancy(1 + h.n_ew, base, &occ), "occupancy");
+    if (occ < 1) throw NxError(NX_ECUDA, "simulation kernel does not fit on an SM");
+    h.per_sm = occ;
+    if (const char* v = std::getenv("NX_SIM_CTAS_PER_SM")) h.per_sm = std::max(1, std::min(occ, std::atoi(v)));
+  }
+  h.slots = std::max(1, std::min(h.n_rep, h.per_sm * sm_count(h.device)));
+  const int64_t scr_stride = nx_refit_scratch_per(h.max_long);
+  scratch_off = static_cast<int64_t>(h.slots) * h.n_ew * scr_stride;
+  const int64_t n_evlog = static_cast<int64_t>(h.slots) * h.max_eng * kEvLogCap;
+  const int64_t n_outbox = static_cast<int64_t>(h.slots) * h.max_eng * h.max_req * 4;
 
   // device arena layout
   Arena A;
@@ -368,6 +424,7 @@ void fill_descriptors(nx_sim& h) {
   h.off_state_begin = align_up(A.size, 256);
 
   const size_t o_kv = A.take<uint8_t>(h.n_req);
+  const size_t o_began = A.take<uint8_t>(h.n_req);
   const size_t o_next = A.take<int>(3 + 2 * 1024);  // kernel scheduling control (nx_state.cuh kSchedCtlInts)
   h.off_state_end = A.size;
   // 0xff-initialised (-1) state
@@ -399,6 +456,10 @@ void fill_descriptors(nx_sim& h) {
   const size_t o_late = A.take<double>(lat_off);
   const size_t o_rec = A.take<int32_t>(h.n_req);
   const size_t o_scr = A.take<double>(scratch_off);
+  const size_t o_evlog = A.take<NxEvLog>(n_evlog);
+  const size_t o_outbox = A.take<int32_t>(n_outbox);
+  const size_t o_pstage = A.take<NxPlanLog>(h.n_plan_log * h.max_eng);
+  const size_t o_lstage = A.take<NxLearnLog>(h.n_learn_log * h.max_eng);
   const size_t o_plog = A.take<NxPlanLog>(h.n_plan_log);
   const size_t o_rlog = A.take<NxRouteLog>(h.n_route_log);
   const size_t o_llog = A.take<NxLearnLog>(h.n_learn_log);
@@ -439,6 +500,16 @@ void fill_descriptors(nx_sim& h) {
   P.sess_engine = reinterpret_cast<int32_t*>(B + o_sess_eng);
   P.records = reinterpret_cast<int32_t*>(B + o_rec);
   P.scratch = reinterpret_cast<double*>(B + o_scr);
+  P.evlog = reinterpret_cast<NxEvLog*>(B + o_evlog);
+  P.outbox = reinterpret_cast<int32_t*>(B + o_outbox);
+  P.plan_stage = reinterpret_cast<NxPlanLog*>(B + o_pstage);
+  P.learn_stage = reinterpret_cast<NxLearnLog*>(B + o_lstage);
+  P.began = reinterpret_cast<uint8_t*>(B + o_began);
+  P.evlog_cap = kEvLogCap;
+  P.outbox_cap = h.max_req;
+  P.scratch_stride = scr_stride;
+  P.slot_engines = h.max_eng;
+  P.slot_warps = h.n_ew;
   P.plan_log = reinterpret_cast<NxPlanLog*>(B + o_plog);
   P.route_log = reinterpret_cast<NxRouteLog*>(B + o_rlog);
   P.learn_log = reinterpret_cast<NxLearnLog*>(B + o_llog);
@@ -507,6 +578,8 @@ const char* site_name(int site) {
 std::string replica_message(const NxReplicaOut& o) {
   if (o.err_site == NX_SITE_PREFILL_CAP)
     return "prefill_priority: prompt exceeds m_max; raise m_max for engine " + std::to_string(o.err_info);
+  if (o.err_site == NX_SITE_OVERFLOW)
+    return std::string(site_name(o.err_site)) + " (code " + std::to_string(o.err_info) + ")";
   return site_name(o.err_site);
 }
 
@@ -593,8 +666,9 @@ int nx_sim_create_json(const char* const* configs, int32_t n_replicas, int32_t d
       for (int i = next++; i < n_replicas; i = next++) {
         codes[i] = guard([&] {
           h->cfgs[i] = nx::parse_run_config(configs[i]);
-          if (h->cfgs[i].engines.size() > NX_MAX_ENGINES)
-            throw std::invalid_argument("device path supports at most 32 engines per replica");
+          // one lane per engine in the router warp's merger, lane 31 for arrivals
+          if (h->cfgs[i].engines.size() > NX_MAX_ENGINES - 1)
+            throw std::invalid_argument("device path supports at most 31 engines per replica");
           check_device_limits(h->cfgs[i], smem_optin);
           h->wl[i] = nx::build_workload(h->cfgs[i]);
           if (h->wl[i].prompt.size() > (1u << 30))
@@ -688,40 +762,33 @@ int nx_sim_launch(nx_sim_t h) {
                                h->off_ff_end - h->off_ff_begin, st), "memset state");
     cuda_check(cudaMemcpyAsync(h->pools.req, h->pools.req0, h->n_req * sizeof(NxReqState),
                                cudaMemcpyDeviceToDevice, st), "request state image");
-    const int spw = static_cast<int>(nx_sim_smem_per_warp(h->max_eng, h->prefix_cap));
-    const size_t smem = static_cast<size_t>(spw);  // per replica CTA
-    int per_sm = 0;
-    cuda_check(nx_sim_occupancy(kWarpsPerBlock, smem, &per_sm), "occupancy");
-    if (per_sm < 1) throw NxError(NX_ECUDA, "simulation kernel does not fit on an SM");
-    // Two replica CTAs per SM: measured 1.76-1.82 s per bench-shard launch vs
-    // 2.04-2.09 s at 3 and 2.17-2.22 s at 4 (the register limit). More
-    // co-resident event loops mostly add instruction-fetch contention
-    // (ncu no_instruction stalls) while the queue of replicas is long enough
-    // to keep two per SM busy (longest first).
-    int cap_sm = 2;
-    if (const char* cap = std::getenv("NX_SIM_CTAS_PER_SM")) cap_sm = std::max(1, std::atoi(cap));
-    per_sm = std::min(per_sm, cap_sm);
-    const int need = h->n_rep;
-    const int grid = std::max(1, std::min(need, per_sm * sm_count(h->device)));
-    // exclusive SMs: the replicas within 10% of the longest expected cost,
-    // when the batch is skewed (longest > 1.5x mean) and fills 2 CTAs on
-    // every SM; at most a quarter of the SMs
-    int n_excl = 0;
-    const int sms = sm_count(h->device);
-    if (per_sm >= 2 && grid >= 2 * sms && h->n_rep > 1) {
-      double mx = 0.0, sum = 0.0;
-      for (double c : h->cost) {
-        mx = std::max(mx, c);
-        sum += c;
-      }
-      if (mx > 1.5 * sum / h->n_rep)
-        for (int i = 0; i < h->n_rep && h->cost[h->order[i]] >= 0.9 * mx; ++i) ++n_excl;
-      n_excl = std::min(n_excl, sms / 4);
+    // one replica CTA per SM (router warp + engine warps use the register
+    // file); the engine warps' fit tables take the shared memory left over
+    const size_t base = nx_sim_smem_per_warp(h->max_eng, h->prefix_cap);
+    int optin = 0, per_sm_smem = 0;
+    cuda_check(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device), "attr");
+    cuda_check(cudaDeviceGetAttribute(&per_sm_smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor, h->device), "attr");
+    int fsm_cap = -1;
+    // per CTA: its share of the SM's shared memory (1 KB reserved per CTA),
+    // minus the kernel's static shared memory
+    size_t room = std::min<size_t>(static_cast<size_t>(optin), static_cast<size_t>(per_sm_smem) / h->per_sm - 1024);
+    room = room > 1024 ? room - 1024 : 0;
+    if (room > base) {
+      const int64_t per = static_cast<int64_t>((room - base) / h->n_ew / sizeof(double)) -
+                          static_cast<int64_t>(nx_sim_fit_table_doubles(0));
+      if (per >= 256) fsm_cap = static_cast<int>(std::min<int64_t>(per, 4096));
     }
-    if (const char* ex = std::getenv("NX_EXCL_SMS")) n_excl = std::max(0, std::min(std::atoi(ex), sms / 2));
-    n_excl = std::min(n_excl, h->n_rep);
-    cuda_check(nx_launch_sim(h->d_pools, h->d_order, h->n_rep, h->d_next, spw, h->prefix_cap, h->max_eng, grid,
-                             kWarpsPerBlock, n_excl, st), "nx_sim_kernel launch");
+    if (const char* fc = std::getenv("NX_FIT_SMEM")) fsm_cap = std::atoi(fc) < 0 ? -1 : std::min(std::atoi(fc), 4096);
+    const size_t smem = base + (fsm_cap >= 0 ? static_cast<size_t>(h->n_ew) * nx_sim_fit_table_doubles(fsm_cap) *
+                                                   sizeof(double)
+                                             : 0);
+    int per_sm = 0;
+    cuda_check(nx_sim_occupancy(1 + h->n_ew, smem, &per_sm), "occupancy");
+    if (per_sm < h->per_sm) throw NxError(NX_ECUDA, "simulation kernel: fewer resident CTAs than planned");
+    const int grid = std::max(1, std::min(h->n_rep, h->slots));
+    arm_debug_dump();
+    cuda_check(nx_launch_sim(h->d_pools, h->d_order, h->n_rep, h->d_next, h->prefix_cap, h->max_eng, h->n_ew,
+                             fsm_cap, smem, grid, st), "nx_sim_kernel launch");
     cuda_check(cudaEventRecord(h->ev1, st), "event");
     h->launched = true;
   });
@@ -750,7 +817,9 @@ int nx_sim_download(nx_sim_t h) {
 
 int nx_sim_synchronize(nx_sim_t h) {
   return guard([&] {
-    cuda_check(cudaStreamSynchronize(h->stream), "nx_sim stream");
+    const cudaError_t se = cudaStreamSynchronize(h->stream);
+    if (se != cudaSuccess) print_debug_dump();
+    cuda_check(se, "nx_sim stream");
     if (h->launched) {
       cuda_check(cudaEventElapsedTime(&h->last_ms, h->ev0, h->ev1), "event time");
       h->launched = false;

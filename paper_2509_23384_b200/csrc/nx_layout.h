@@ -9,6 +9,7 @@
 
 #define NX_MAX_ENGINES 32      /* one lane per engine in the warp-wide scans */
 #define NX_TW_CAP 200          /* TradeoffEstimator::kWindow, proj/include/servesim/lens.h:145 */
+#define NX_EVLOG_CAP (1 << 15) /* event-log ring entries per engine (power of two) */
 
 /* Per-engine static description + pool offsets (one per engine, all replicas). */
 typedef struct NxEngineDesc {
@@ -105,6 +106,17 @@ typedef struct NxReqState {
   int32_t prefilled, decoded, prompt, target;
 } NxReqState;
 
+/* One logged event of an engine's stream (the engine-parallel event loop,
+   device/sim_kernel.cu): its time, a reference to the event that pushed it
+   (its parent: a log index in the same engine's stream, or a root event's
+   sequence number) and its kind + flags. The reference's (time, sequence)
+   order is recovered from these references (sim.cpp:50-55, 67-70). */
+typedef struct NxEvLog {
+  int64_t t;
+  uint32_t par;
+  uint32_t meta;
+} NxEvLog;
+
 /* Device pools (all pointers are device pointers). */
 typedef struct NxPools {
   /* request inputs */
@@ -124,7 +136,15 @@ typedef struct NxPools {
   double* lat_t; double* lat_e2e;
   int32_t* sess_engine;
   int32_t* records;
-  double* scratch;
+  double* scratch;               /* learner scratch: per CTA slot x engine warp */
+  /* engine-parallel event loop, per CTA slot x engine (capacities below) */
+  NxEvLog* evlog;                /* event-log ring per engine */
+  int32_t* outbox;               /* completed requests per engine, 4 ints each */
+  NxPlanLog* plan_stage;         /* per replica x engine plan rows (logging only) */
+  NxLearnLog* learn_stage;       /* per replica x engine learner rows (logging only) */
+  uint8_t* began;                /* per request: its arrival started a step (plan logging) */
+  int64_t evlog_cap, outbox_cap, scratch_stride;
+  int32_t slot_engines, slot_warps;  /* engines / engine warps per CTA slot */
   NxPlanLog* plan_log; NxRouteLog* route_log; NxLearnLog* learn_log;
   /* descriptors + outputs */
   const NxReplicaDesc* rep; const NxEngineDesc* eng;

@@ -91,7 +91,9 @@ def test_two_rank_shards_through_the_library_equal_one_process(tmp_path):
     assert all(s.status == 0 for s in sums)
     got[:, STAMP] = 0
     want[:, STAMP] = 0
-    assert np.array_equal(got, want)
+    diff = sorted(set(np.nonzero(got != want)[1].tolist()))
+    assert np.array_equal(got, want), f"differing byte offsets {diff}"
+
     # the records carry the event hashes the single-process run reports
     eh = got[:, 40:48].copy().view(np.uint64).ravel()
     assert [int(x) for x in eh] == [s.event_hash for s in sums]

@@ -1545,6 +1545,7 @@ static __device__ NX_COLD void record_sample(Ctx& c, int e, int b, int s, double
     // engine-parallel loop: the engine's own warp refits (its timeline waits
     // for the new params anyway; other engines' warps keep running)
 #ifdef NX_INLINE_REFIT
+    if (nx_timers_on && c.lane == 0) c.rs->lcycles[3] = 1;  // window attribution (tools/merge_probe.py)
     PhaseTimer pt(c.rs, 6);
     update_structural(c, e);
 #else

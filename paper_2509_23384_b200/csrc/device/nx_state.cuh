@@ -169,6 +169,8 @@ struct Ctx {
   int32_t* obox;           // this CTA slot's outboxes
   int64_t ob_cap;          // outbox entries per engine
   NxEvLog* sring;          // shared-memory copies of the rings' most recent entries
+  NxReqState* req;         // this replica's request state (shared memory or HBM)
+  uint8_t* kva;            // this replica's KV-admitted flags (shared memory or HBM)
 };
 
 template <class T>

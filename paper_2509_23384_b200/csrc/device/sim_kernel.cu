@@ -78,7 +78,7 @@ __device__ __forceinline__ int rr_mod(uint64_t rr, int n) {
                            : static_cast<int>(rr % static_cast<uint64_t>(n));
 }
 __device__ __forceinline__ int remaining(const Ctx& c, int r) {
-  return c.P->req[c.roff + r].prompt - c.P->req[c.roff + r].prefilled;
+  return c.req[r].prompt - c.req[r].prefilled;
 }
 
 // target_latency (lens.cpp:10-31) with the engine's tradeoff model
@@ -251,17 +251,17 @@ __device__ NX_COLD void trim_for_kv(Ctx& c, int e) {
       const int r = preq[k];
       const int tok = ptok[k];
       bool keep;
-      if (tok < 0 || c.P->kv_admitted[c.roff + r]) {
+      if (tok < 0 || c.kva[r]) {
         keep = true;
       } else if (trimmed) {
         keep = false;
       } else {
-        const int foot = blocks_for(c.P->req[c.roff + r].prompt + c.P->req[c.roff + r].target, ed.block_size);
-        const int fut = foot - blocks_for(c.P->req[c.roff + r].prefilled + c.P->req[c.roff + r].decoded,
+        const int foot = blocks_for(c.req[r].prompt + c.req[r].target, ed.block_size);
+        const int fut = foot - blocks_for(c.req[r].prefilled + c.req[r].decoded,
                                           ed.block_size);
         if (static_cast<int64_t>(g.pinned) + g.reserved + fut <= ed.kv_blocks) {
           g.reserved += fut;
-          c.P->kv_admitted[c.roff + r] = 1;
+          c.kva[r] = 1;
           keep = true;
         } else {
           trimmed = true;
@@ -438,13 +438,13 @@ __device__ bool admit(Ctx& c, int e, int r) {
   const int sess = c.P->session[c.roff + r];
   const int cached = L.tok[sess];
   if (cached >= 0) {
-    const int prompt = c.P->req[c.roff + r].prompt;
+    const int prompt = c.req[r].prompt;
     const int credit = cached < prompt - 1 ? cached : prompt - 1;
     const int cb = blocks_for(credit, ed.block_size);
     if (credit > 0 && static_cast<int64_t>(g.pinned) + g.reserved + cb <= ed.kv_blocks) {
       g.cache_blocks -= blocks_for(cached, ed.block_size);
       lru_unlink(g, L, sess);
-      c.P->req[c.roff + r].prefilled = credit;
+      c.req[r].prefilled = credit;
       g.pinned += cb;
     }
   }
@@ -525,14 +525,14 @@ __device__ NX_COLD void step_complete(Ctx& c, int e, int64_t now_us) {
     if (k < n) {
       r = preq[k];
       const int tok = ptok[k];
-      const int4 q = *reinterpret_cast<const int4*>(&P.req[ro + r]);  // one 16-B load
+      const int4 q = *reinterpret_cast<const int4*>(&c.req[r]);  // one 16-B load
       int pre = q.x, dec = q.y;
       const int before = blocks_for(pre + dec, block);
       if (tok >= 0) pre += tok;
       else dec += 1;
       const int after = blocks_for(pre + dec, block);
       delta = after - before;
-      *reinterpret_cast<int2*>(&P.req[ro + r]) = make_int2(pre, dec);
+      *reinterpret_cast<int2*>(&c.req[r]) = make_int2(pre, dec);
       first = tok >= 0 && pre == q.z;
       fin = tok < 0 && dec == q.w;
       if (first) P.first_us[ro + r] = now_us;
@@ -566,7 +566,7 @@ __device__ NX_COLD void step_complete(Ctx& c, int e, int64_t now_us) {
           const int rr = st_req[l];
           cache_insert(g, L, st_sess[l], st_tok[l], ed.kv_blocks, st_pin[l], block);
           // CompletionStats + TradeoffEstimator EMA/window (lens.cpp:149-160)
-          const int tgt = P.req[ro + rr].target;
+          const int tgt = c.req[rr].target;
           const double first_ms = to_ms(P.first_us[ro + rr]);
           const double ttft = first_ms - P.arr_ms[ro + rr];
           const double tpot = tgt >= 2 ? (now - first_ms) / static_cast<double>(tgt - 1) : 0.0;
@@ -630,7 +630,7 @@ __device__ NX_COLD void step_complete(Ctx& c, int e, int64_t now_us) {
     for (int base = 0; base < len; base += 32) {
       const int i = base + c.lane;
       const int r = i < len ? rq[i] : 0;
-      const bool keep = i < len && P.req[ro + r].decoded != P.req[ro + r].target;
+      const bool keep = i < len && c.req[r].decoded != c.req[r].target;
       const unsigned m = __ballot_sync(NX_FULL, keep);
       __syncwarp();
       if (keep) rq[out + __popc(m & ((1u << c.lane) - 1))] = r;
@@ -646,7 +646,7 @@ __device__ NX_COLD void step_complete(Ctx& c, int e, int64_t now_us) {
       int r = 0;
       if (k < n && ptok[k] >= 0) {
         r = preq[k];
-        nr = P.req[ro + r].prefilled == P.req[ro + r].prompt;
+        nr = c.req[r].prefilled == c.req[r].prompt;
       }
       const unsigned m = __ballot_sync(NX_FULL, nr);
       if (nr) rq[out + __popc(m & ((1u << c.lane) - 1))] = r;
@@ -660,7 +660,7 @@ __device__ NX_COLD void step_complete(Ctx& c, int e, int64_t now_us) {
       int wpos = head + span - 1;
       for (int i = span - 1; i >= 0; --i) {
         const int r = wq[head + i];
-        if (P.req[ro + r].prefilled != P.req[ro + r].prompt) wq[wpos--] = r;
+        if (c.req[r].prefilled != c.req[r].prompt) wq[wpos--] = r;
       }
       const int removed = wpos + 1 - head;
       g.wq_head = head + removed;
@@ -849,7 +849,7 @@ __device__ NX_COLD int route(Ctx& c, int rid, double now, double& score, double 
       break;
     }
     default: {  // PRISM multiplicative score (router.cpp:205-284)
-      const int prompt = c.P->req[c.roff + rid].prompt;
+      const int prompt = c.req[rid].prompt;
       const double dem = static_cast<double>(prompt) + c.rs->l_bar_ema;
       const double demand = (1.0 < dem) ? dem : 1.0;
       const int e = c.lane;
@@ -1610,6 +1610,7 @@ __device__ NX_COLD void router_warp(Ctx& c, int n_ew) {
   const long long tw0 = nx_clock();
   while (!vload(R.final_mode)) {
     if (nx_timers_on && c.lane == 0) R.cycles[kTmNWindows] += 1;
+    const long long twin = nx_clock();
     // merge behind the engines until every engine warp has parked
     long long t0 = nx_globaltimer();
     while (true) {
@@ -1624,6 +1625,15 @@ __device__ NX_COLD void router_warp(Ctx& c, int n_ew) {
       }
     }
     __threadfence_block();
+    if (nx_timers_on && c.lane == 0) {  // window wall, and how much of it had a structural refit
+      const long long dt = nx_clock() - twin;
+      R.lcycles[6] += dt;
+      if (R.lcycles[3]) {
+        R.lcycles[4] += dt;
+        R.lcycles[5] += 1;
+        R.lcycles[3] = 0;
+      }
+    }
     {
       const long long tc = nx_clock();
       while (merge_some(c, 1 << 30) > 0) {
@@ -1776,8 +1786,10 @@ __device__ NX_COLD void write_outputs(Ctx& c, int r, int n_warps) {
     o.err_info = err.info;
     for (int i = 0; i < 6; ++i) o.work[i] = R.work[i];
     for (int i = 0; i < 16; ++i) o.cycles[i] = R.cycles[i];
-    if (nx_timers_on == 2)  // merger counters instead of the phase-wall slots
-      for (int i = 0; i < 4; ++i) o.cycles[12 + i] = R.lcycles[i];
+    if (nx_timers_on == 2)  // window counters instead of the phase-wall slots
+      for (int i = 0; i < 4; ++i) o.cycles[12 + i] = R.lcycles[4 + i];
+    if (nx_timers_on == 3)  // learner-internal timers in slots 8..15
+      for (int i = 8; i < 16; ++i) o.cycles[i] = R.lcycles[i == 8 ? 7 : i];
     o.t_begin_ns = R.t_begin_ns;
     o.n_plan_log = R.n_plan_log;
     o.n_route_log = R.n_route_log;
@@ -1817,7 +1829,7 @@ __host__ __device__ __forceinline__ size_t sim_smem_base(int max_eng, int prefix
 // indices (host order, longest expected first) from a global counter.
 extern "C" __global__ void __launch_bounds__(32 * nxd::kPdMaxWarps, 1)
 nx_sim_kernel(const NxPools* __restrict__ pools, const int32_t* __restrict__ order, int n_rep,
-              int* ctl, int prefix_cap, int max_eng, int n_ew, int fsm_cap) {
+              int* ctl, int prefix_cap, int max_eng, int n_ew, int fsm_cap, int req_cap) {
   using namespace nxd;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int s_slot;
@@ -1837,6 +1849,13 @@ nx_sim_kernel(const NxPools* __restrict__ pools, const int32_t* __restrict__ ord
   off += align16(sizeof(EngSm) * static_cast<size_t>(max_eng));
   c.sring = reinterpret_cast<NxEvLog*>(smem + off);
   off += sizeof(NxEvLog) * kRing * static_cast<size_t>(max_eng);
+  // request state (prefilled, decoded, prompt, target) + KV-admitted flags of
+  // the replica in shared memory when it fits (req_cap requests), else in HBM
+  NxReqState* sreq = reinterpret_cast<NxReqState*>(smem + off);
+  off += sizeof(NxReqState) * static_cast<size_t>(req_cap);
+  uint8_t* skva = smem + off;
+  off += align16(static_cast<size_t>(req_cap));
+
   c.fsm = (warp > 0 && fsm_cap >= 0)
               ? reinterpret_cast<double*>(smem + off) + static_cast<size_t>(warp - 1) * (kFbTable + fsm_cap)
               : nullptr;
@@ -1870,6 +1889,17 @@ nx_sim_kernel(const NxPools* __restrict__ pools, const int32_t* __restrict__ ord
     c.roff = c.d->req_off;
     c.soff = c.d->sess_off;
     c.lin_rows = c.scratch + 6 * c.d->long_w + kFbTable;
+    if (c.n_req <= req_cap) {
+      c.req = sreq;
+      c.kva = skva;
+      for (int i = threadIdx.x; i < c.n_req; i += blockDim.x) {
+        sreq[i] = pools->req0[c.roff + i];
+        skva[i] = 0;
+      }
+    } else {
+      c.req = pools->req + c.roff;
+      c.kva = pools->kv_admitted + c.roff;
+    }
     if (warp == 0) init_replica(c, n_warps);
     __syncthreads();
     if (warp == 0) router_warp(c, n_ew);
@@ -1886,16 +1916,19 @@ extern "C" size_t nx_sim_smem_per_warp(int max_engines, int prefix_cap) {
   return nxd::sim_smem_base(max_engines, prefix_cap);
 }
 // Doubles of one engine warp's shared-memory fit tables for fsm_cap 1/f_S entries.
+extern "C" size_t nx_sim_req_smem_bytes(int req_cap) {
+  return sizeof(NxReqState) * static_cast<size_t>(req_cap) + nxd::align16(static_cast<size_t>(req_cap));
+}
 extern "C" size_t nx_sim_fit_table_doubles(int fsm_cap) {
   return static_cast<size_t>(nxd::kFbTable + fsm_cap);
 }
 
 extern "C" cudaError_t nx_launch_sim(const NxPools* d_pools, const int32_t* d_order, int n_rep,
                                      int* d_next, int prefix_cap, int max_eng, int n_ew, int fsm_cap,
-                                     size_t smem, int grid, cudaStream_t st) {
+                                     int req_cap, size_t smem, int grid, cudaStream_t st) {
 #ifdef NX_TIMERS
   const char* tm = getenv("NX_PHASE_TIMERS");
-  const int timers = tm ? (tm[0] == '1' ? 1 : tm[0] == '2' ? 2 : 0) : 0;
+  const int timers = tm ? (tm[0] >= '1' && tm[0] <= '3' ? tm[0] - '0' : 0) : 0;
   cudaError_t terr = cudaMemcpyToSymbolAsync(nxd::nx_timers_on, &timers, sizeof timers, 0,
                                              cudaMemcpyHostToDevice, st);
   if (terr != cudaSuccess) return terr;
@@ -1904,7 +1937,7 @@ extern "C" cudaError_t nx_launch_sim(const NxPools* d_pools, const int32_t* d_or
                                          static_cast<int>(smem));
   if (err != cudaSuccess) return err;
   nx_sim_kernel<<<grid, 32 * (1 + n_ew), smem, st>>>(d_pools, d_order, n_rep, d_next, prefix_cap, max_eng, n_ew,
-                                                      fsm_cap);
+                                                      fsm_cap, req_cap);
   return cudaGetLastError();
 }
 

@@ -30,8 +30,9 @@
 
 extern "C" cudaError_t nx_launch_sim(const NxPools* d_pools, const int32_t* d_order, int n_rep,
                                      int* d_next, int prefix_cap, int max_eng, int n_ew, int fsm_cap,
-                                     size_t smem, int grid, cudaStream_t st);
+                                     int req_cap, size_t smem, int grid, cudaStream_t st);
 extern "C" size_t nx_sim_fit_table_doubles(int fsm_cap);
+extern "C" size_t nx_sim_req_smem_bytes(int req_cap);
 extern "C" cudaError_t nx_sim_set_debug(unsigned long long* dev_ptr);
 
 namespace {
@@ -764,7 +765,7 @@ int nx_sim_launch(nx_sim_t h) {
                                cudaMemcpyDeviceToDevice, st), "request state image");
     // one replica CTA per SM (router warp + engine warps use the register
     // file); the engine warps' fit tables take the shared memory left over
-    const size_t base = nx_sim_smem_per_warp(h->max_eng, h->prefix_cap);
+    size_t base = nx_sim_smem_per_warp(h->max_eng, h->prefix_cap);
     int optin = 0, per_sm_smem = 0;
     cuda_check(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device), "attr");
     cuda_check(cudaDeviceGetAttribute(&per_sm_smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor, h->device), "attr");
@@ -773,6 +774,14 @@ int nx_sim_launch(nx_sim_t h) {
     // minus the kernel's static shared memory
     size_t room = std::min<size_t>(static_cast<size_t>(optin), static_cast<size_t>(per_sm_smem) / h->per_sm - 1024);
     room = room > 1024 ? room - 1024 : 0;
+    // request state in shared memory when the largest replica's fits in a
+    // quarter of the room (17 B per request); else it stays in HBM
+    int req_cap = 0;
+    if (const size_t need = nx_sim_req_smem_bytes(static_cast<int>(h->max_req)); base + need <= room / 4 + base &&
+        need <= room / 4)
+      req_cap = static_cast<int>(h->max_req);
+    if (const char* v = std::getenv("NX_REQ_SMEM")) if (v[0] == '0') req_cap = 0;
+    base += nx_sim_req_smem_bytes(req_cap);
     if (room > base) {
       const int64_t per = static_cast<int64_t>((room - base) / h->n_ew / sizeof(double)) -
                           static_cast<int64_t>(nx_sim_fit_table_doubles(0));
@@ -788,7 +797,7 @@ int nx_sim_launch(nx_sim_t h) {
     const int grid = std::max(1, std::min(h->n_rep, h->slots));
     arm_debug_dump();
     cuda_check(nx_launch_sim(h->d_pools, h->d_order, h->n_rep, h->d_next, h->prefix_cap, h->max_eng, h->n_ew,
-                             fsm_cap, smem, grid, st), "nx_sim_kernel launch");
+                             fsm_cap, req_cap, smem, grid, st), "nx_sim_kernel launch");
     cuda_check(cudaEventRecord(h->ev1, st), "event");
     h->launched = true;
   });

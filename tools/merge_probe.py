@@ -1,9 +1,18 @@
-import os,sys
-os.environ["NX_PHASE_TIMERS"]="2"; os.environ["NX_SO"]="/root/repo/tools/_timers/_nxsched.so"
-sys.path.insert(0,"/root/repo")
+"""Window attribution (NX_PHASE_TIMERS=2 diagnostic build): wall of the
+arrival windows, and the part spent in windows where an engine ran a
+structural refit."""
+import os, sys
+os.environ["NX_PHASE_TIMERS"] = "2"
+os.environ.setdefault("NX_SO", os.path.join(os.path.dirname(os.path.abspath(__file__)), "_timers", "_nxsched.so"))
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
 from paper_2509_23384_b200 import sim, workloads as W
-cfgs=[W.sweep_replica(r,1,p,2000) for r in (10.0,47.5) for p in ("prism",)]
-b=sim.Batch(cfgs); b.run()
-for i,c in enumerate(cfgs):
-    cy=b.phase_cycles(i); s=b.summaries()[i]
-    print(c['workload']['rate'], "events",s.events,"merge_s",cy[0]/1.965e9,"calls",cy[12],"merged",cy[13],"empty",cy[14],"catchup_s",cy[15]/1.965e9)
+HZ = 1.965e9
+cfgs = [W.sweep_replica(r, 1, p, 2000) for r in (10.0, 25.0, 47.5) for p in ("prism", "round_robin")]
+b = sim.Batch(cfgs)
+b.run()
+for i, c in enumerate(cfgs):
+    cy = b.phase_cycles(i)
+    t0, t1 = b.timeline(i)
+    print(f"rate {c['workload']['rate']:5.1f} {c['router']['policy']:12s} wall {(t1 - t0) / 1e9:.3f}s "
+          f"windows {cy[14] / HZ:.3f}s of which refit windows {cy[12] / HZ:.3f}s ({cy[13]} windows) "
+          f"structural(sum) {cy[6] / HZ:.3f}s events(sum) {cy[10] / HZ:.3f}s")

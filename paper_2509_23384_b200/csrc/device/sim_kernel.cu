@@ -32,6 +32,9 @@
 #define NX_COMPACT_MATH 1  // one out-of-line expm1 (was ~180 KB of inlined copies)
 #endif
 #define NX_INLINE_REFIT 1  // structural refits run on the engine's own warp (record_sample)
+#ifndef NX_SIM_LB_WARPS
+#define NX_SIM_LB_WARPS 9  // warps per replica CTA the register budget is sized for (router + engine warps)
+#endif
 #include <stdlib.h>
 
 #include "nx_learner.cuh"
@@ -1827,7 +1830,7 @@ __host__ __device__ __forceinline__ size_t sim_smem_base(int max_eng, int prefix
 // One CTA per replica: warp 0 is the router (arrivals, merger), warps
 // 1..n_ew each own the engines e with e % n_ew == warp - 1. CTAs pull replica
 // indices (host order, longest expected first) from a global counter.
-extern "C" __global__ void __launch_bounds__(32 * nxd::kPdMaxWarps, 1)
+extern "C" __global__ void __launch_bounds__(32 * NX_SIM_LB_WARPS, 1)
 nx_sim_kernel(const NxPools* __restrict__ pools, const int32_t* __restrict__ order, int n_rep,
               int* ctl, int prefix_cap, int max_eng, int n_ew, int fsm_cap, int req_cap) {
   using namespace nxd;

@@ -53,26 +53,26 @@ __device__ __forceinline__ double expm1_neg(double kx) { return -expm1(-kx); }
 // below 1e-17 relative). Within ~1 ulp of the correctly rounded value; K1's
 // contract is 1e-9 relative in fp64 mode, and the simulator keeps libm's
 // expm1 (bit-for-bit decisions are certified against it).
+// Coefficients in the constant bank: a DFMA reads a c[bank][offset] operand
+// directly, while an inline FP64 immediate costs two UMOVs per use (the K1
+// loop issued more UMOVs than DFMAs before).
+static __constant__ double kOmeC[16] = {
+    1.4426950408889634,          // 1 / ln2
+    6.93147180369123816490e-01,  // ln2 hi
+    1.90821492927058770002e-10,  // ln2 lo
+    1.0 / 6227020800.0, 1.0 / 479001600.0, 1.0 / 39916800.0, 1.0 / 3628800.0, 1.0 / 362880.0,
+    1.0 / 40320.0, 1.0 / 5040.0, 1.0 / 720.0, 1.0 / 120.0, 1.0 / 24.0, 1.0 / 6.0, 0.5, 1.0};
 __device__ __forceinline__ double one_minus_exp_neg(double x) {
   const double y = -x;
-  const double kd = rint(y * 1.4426950408889634);           // y / ln2
-  const double r0 = fma(-kd, 6.93147180369123816490e-01, y); // ln2 hi
-  const double r = fma(-kd, 1.90821492927058770002e-10, r0); // ln2 lo
-  double p = 1.0 / 6227020800.0;                             // 1/13!
-  p = fma(p, r, 1.0 / 479001600.0);
-  p = fma(p, r, 1.0 / 39916800.0);
-  p = fma(p, r, 1.0 / 3628800.0);
-  p = fma(p, r, 1.0 / 362880.0);
-  p = fma(p, r, 1.0 / 40320.0);
-  p = fma(p, r, 1.0 / 5040.0);
-  p = fma(p, r, 1.0 / 720.0);
-  p = fma(p, r, 1.0 / 120.0);
-  p = fma(p, r, 1.0 / 24.0);
-  p = fma(p, r, 1.0 / 6.0);
-  p = fma(p, r, 0.5);
-  const double em = fma(r * r, p, r);                        // expm1(r)
+  const double kd = rint(y * kOmeC[0]);                    // y / ln2
+  const double r0 = fma(-kd, kOmeC[1], y);                 // ln2 hi
+  const double r = fma(-kd, kOmeC[2], r0);                 // ln2 lo
+  double p = kOmeC[3];                                     // 1/13!
+#pragma unroll
+  for (int i = 4; i < 15; ++i) p = fma(p, r, kOmeC[i]);    // ... 1/3!, 1/2
+  const double em = fma(r * r, p, r);                      // expm1(r)
   const double s = __longlong_as_double(static_cast<long long>(1023 + static_cast<int>(kd)) << 52);  // 2^k
-  return fma(-s, em, 1.0 - s);                               // -(2^k em + 2^k - 1)
+  return fma(-s, em, kOmeC[15] - s);                       // -(2^k em + 2^k - 1)
 }
 __device__ __forceinline__ double sat_fast(double k, double x) {
   const double kx = k * x;

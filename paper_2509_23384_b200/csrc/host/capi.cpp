@@ -793,8 +793,10 @@ int nx_sim_launch(nx_sim_t h) {
                                              : 0);
     int per_sm = 0;
     cuda_check(nx_sim_occupancy(1 + h->n_ew, smem, &per_sm), "occupancy");
-    if (per_sm < h->per_sm) throw NxError(NX_ECUDA, "simulation kernel: fewer resident CTAs than planned");
-    const int grid = std::max(1, std::min(h->n_rep, h->slots));
+    if (per_sm < 1) throw NxError(NX_ECUDA, "simulation kernel does not fit on an SM");
+    // (the slots were planned without the request state's shared memory: a
+    // launch that fits fewer CTAs per SM uses fewer of them)
+    const int grid = std::max(1, std::min({h->n_rep, h->slots, std::min(per_sm, h->per_sm) * sm_count(h->device)}));
     arm_debug_dump();
     cuda_check(nx_launch_sim(h->d_pools, h->d_order, h->n_rep, h->d_next, h->prefix_cap, h->max_eng, h->n_ew,
                              fsm_cap, req_cap, smem, grid, st), "nx_sim_kernel launch");

@@ -52,6 +52,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-operators", action="store_true", help="skip the batched K2/K3/K4 lines")
+    ap.add_argument("--no-traffic", action="store_true",
+                    help="skip the in-run ncu DRAM-traffic probe (roofline.traffic from profiles/ instead)")
+    ap.add_argument("--traffic-probe", action="store_true", help=argparse.SUPPRESS)
     return ap.parse_args()
 
 
@@ -193,14 +196,82 @@ TRAFFIC_SOURCE = (f"profiles/{TRAFFIC_FILE}: dram__bytes_read.sum + dram__bytes_
                   "ncu --set full capture of this build (not re-measured in this run)")
 
 
+_TRAFFIC = {}  # measured in this run (probe_traffic), else the committed capture
+
+
 def traffic(kernel: str):
-    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel`
-    from the committed ncu --set full capture of the current build."""
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel`:
+    measured in this run by the ncu probe when it ran, else from the committed
+    ncu --set full capture of the current build."""
+    if kernel in _TRAFFIC:
+        return _TRAFFIC[kernel]
     try:
         t = json.loads((ROOT / "profiles" / TRAFFIC_FILE).read_text())
         return t[kernel]["traffic_bytes_per_launch"]
     except Exception:
         return None
+
+
+def probe_traffic(args) -> str:
+    """One launch of the bench-shard simulation and of K1 under
+    `ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum` (a child
+    process: a profiled launch is never a timed one), same box, same build.
+    Fills _TRAFFIC; returns a description for roofline.traffic_source."""
+    import shutil
+    import subprocess
+    ncu = shutil.which("ncu") or "/usr/local/cuda/bin/ncu"
+    if not Path(ncu).exists():
+        return TRAFFIC_SOURCE + " (ncu not found for the in-run probe)"
+    cmd = [ncu, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum", "--clock-control", "none",
+           "--print-units", "base", "--csv", "-k", "regex:nx_sim_kernel|perf_eval_kernel",
+           sys.executable, str(ROOT / "bench.py"), "--traffic-probe",
+           "--replicas-per-gpu", str(args.replicas_per_gpu), "--requests", str(args.requests)]
+    try:
+        out = subprocess.run(cmd, capture_output=True, text=True, timeout=600).stdout
+    except Exception as exc:  # noqa: BLE001 — the committed capture stays the fallback
+        return TRAFFIC_SOURCE + f" (in-run probe failed: {exc!r})"
+    import csv
+    import io
+    got = {}
+    rows = [r for r in csv.reader(io.StringIO(out)) if len(r) > 5]
+    if rows:
+        hdr = rows[0]
+        try:
+            kn, mn, mv = hdr.index("Kernel Name"), hdr.index("Metric Name"), hdr.index("Metric Value")
+            for r in rows[1:]:
+                k = "nx_sim_kernel" if "nx_sim_kernel" in r[kn] else (
+                    "perf_eval_kernel" if "perf_eval_kernel" in r[kn] else None)
+                if k and r[mn].startswith("dram__bytes_"):
+                    got.setdefault(k, {})[r[mn]] = float(r[mv].replace(",", ""))
+        except ValueError:
+            got = {}
+    for k, m in got.items():
+        if len(m) == 2:
+            _TRAFFIC[k] = int(sum(m.values()))
+    if not _TRAFFIC:
+        return TRAFFIC_SOURCE + " (in-run probe returned no counters)"
+    return ("measured in this run: dram__bytes_read.sum + dram__bytes_write.sum of one launch of the "
+            "same workload under ncu --clock-control none (child process, not timed)")
+
+
+def traffic_probe_child(args):
+    """The ncu child of probe_traffic: one shard launch, one K1 launch."""
+    import torch
+    from paper_2509_23384_b200 import perf_model, sim
+    dev = torch.device("cuda", 0)
+    b = sim.Batch(shard_configs(0, args.replicas_per_gpu, args.requests))
+    b.run()
+    b.close()
+    n = 1 << 26
+    g = torch.Generator(device=dev).manual_seed(5)
+    params = perf_model.profile_table(dev)
+    idx = torch.randint(0, params.shape[0], (n,), device=dev, dtype=torch.int32, generator=g)
+    bb = torch.randint(1, 257, (n,), device=dev, dtype=torch.int32, generator=g)
+    ss = bb + torch.randint(0, 8192, (n,), device=dev, dtype=torch.int32, generator=g)
+    out = torch.empty(n, device=dev, dtype=torch.float64)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    perf_model.eval_device_async(params, idx, bb, ss, out, status, stream=torch.cuda.current_stream(dev))
+    torch.cuda.synchronize(dev)
 
 
 def baseline_configs_line(torch, local: int) -> dict:
@@ -550,6 +621,9 @@ def run_nx(args):
         gathered = world * len(cfgs)
 
     # roofline of the dominant kernel (nx_sim_kernel), from device work counters
+    traffic_source = TRAFFIC_SOURCE
+    if rank == 0 and world == 1 and not args.no_traffic:
+        traffic_source = probe_traffic(args)
     pk, src = peaks()
     alg = algorithmic_bytes(batch, len(cfgs))
     per_launch_s = kernel_s / args.steps
@@ -566,12 +640,13 @@ def run_nx(args):
             "gpu_launches": args.steps,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                          "frac": achieved / pk["hbm_gbs"], "traffic": traffic("nx_sim_kernel"),
-                         "traffic_source": TRAFFIC_SOURCE,
+                         "traffic_source": traffic_source,
                          "kernel": "nx_sim_kernel", "peak_source": src,
                          "algorithmic_bytes_per_launch": alg,
-                         "limiter": "latency: one dependent event chain per replica (FP64 model "
-                                    "evaluations, shared-memory state); HBM is not the bound "
-                                    "(DESIGN.md §5)"},
+                         "limiter": "latency, not HBM: a replica's critical path is the sum over its "
+                                    "arrival windows of the slowest engine warp's events (structural "
+                                    "refits about half of it); the achieved GB/s is algorithmic bytes "
+                                    "over that time (DESIGN.md §5)"},
             "clocks": clk.summary(),
         }
         if e2e:
@@ -620,6 +695,9 @@ def run_nx(args):
 
 def main():
     args = parse()
+    if args.traffic_probe:
+        traffic_probe_child(args)
+        return
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -1,0 +1,26 @@
+"""Per-call latency of the scalar drop-in calls (each one a device round
+trip) vs their batched forms."""
+import sys, time
+from pathlib import Path
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import numpy as np
+from paper_2509_23384_b200 import perf_model as pm, lens
+p = pm.PROFILES["fast"]
+for _ in range(50):
+    pm.predict_latency(p, (4, 100))
+n = 2000
+t0 = time.perf_counter()
+for i in range(n):
+    pm.predict_latency(p, (4, 100 + i))
+t1 = time.perf_counter()
+print(f"predict_latency (scalar, ctypes): {1e6 * (t1 - t0) / n:.1f} us/call")
+rows = [p]
+N = 1 << 20
+rng = np.random.default_rng(1)
+b = rng.integers(1, 256, N); s = b + rng.integers(0, 8000, N); idx = np.zeros(N, dtype=np.int64)
+pm.eval_host(rows, idx, b, s)
+t0 = time.perf_counter()
+for _ in range(5):
+    pm.eval_host(rows, idx, b, s)
+t1 = time.perf_counter()
+print(f"predict_latency batched from host arrays (2^20 records incl. H2D/D2H): {1e9 * (t1 - t0) / 5 / N:.2f} ns/record")

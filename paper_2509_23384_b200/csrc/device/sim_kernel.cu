@@ -1641,7 +1641,7 @@ __device__ NX_COLD void router_warp(Ctx& c, int n_ew) {
       const long long tc = nx_clock();
       while (merge_some(c, 1 << 30) > 0) {
       }
-      if (nx_timers_on && c.lane == 0) R.lcycles[3] += nx_clock() - tc;
+      if (nx_timers_on && c.lane == 0) R.lcycles[7] += nx_clock() - tc;  // merge catch-up at the barrier
     }
     bool err = false;
     for (int w = 1; w <= n_ew; ++w) err |= R.err[w].status != 0;

@@ -637,7 +637,7 @@ def run_nx(args):
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": workload_desc(args.replicas_per_gpu, args.requests, world),
             "decisions_per_step": total_dec / args.steps,
-            "gpu_launches": args.steps,
+            "gpu_launches": 2 * args.steps,  # nx_sim_kernel + nx_summarize_kernel per launch
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                          "frac": achieved / pk["hbm_gbs"], "traffic": traffic("nx_sim_kernel"),
                          "traffic_source": traffic_source,

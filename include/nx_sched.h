@@ -331,6 +331,15 @@ int nx_sim_io_bytes(nx_sim_t h, int64_t* h2d, int64_t* d2h);
 int nx_sim_replica_count(nx_sim_t h);
 int nx_sim_summaries(nx_sim_t h, nx_replica_summary* out);
 /* Byte-identical to RunResult::summary_json (proj/src/sim.cpp:349-392). */
+/* servesim::MetricsSummary of one replica (metrics.h / metrics.cpp:40-91),
+ * computed on the device after the run (K7, device/summary.cu): nearest-rank
+ * percentiles by radix selection, the means as the reference's left folds. */
+typedef struct nx_replica_metrics {
+  int64_t completed;
+  double p50_e2e_ms, p90_e2e_ms, p50_ttft_ms, p50_tpot_ms;
+  double mean_ttft_ms, mean_tpot_ms, slo_attainment_pct;
+} nx_replica_metrics;
+int nx_sim_metrics(nx_sim_t h, int32_t replica, nx_replica_metrics* out);
 int nx_sim_summary_json(nx_sim_t h, int32_t replica, char* buf, int64_t cap, int64_t* len);
 int nx_sim_records(nx_sim_t h, int32_t replica, nx_request_record* out, int64_t cap,
                    int64_t* n);

@@ -31,6 +31,12 @@ class ReplicaSummary(C.Structure):
                 ("status", C.c_int32), ("err_site", C.c_int32)]
 
 
+class ReplicaMetrics(C.Structure):  # nx_replica_metrics (servesim::MetricsSummary)
+    _fields_ = [("completed", C.c_int64), ("p50_e2e_ms", C.c_double), ("p90_e2e_ms", C.c_double),
+                ("p50_ttft_ms", C.c_double), ("p50_tpot_ms", C.c_double), ("mean_ttft_ms", C.c_double),
+                ("mean_tpot_ms", C.c_double), ("slo_attainment_pct", C.c_double)]
+
+
 class RequestRecord(C.Structure):
     _fields_ = [("request_id", C.c_int64), ("arrival_ms", C.c_double),
                 ("first_token_ms", C.c_double), ("completed_ms", C.c_double),
@@ -79,6 +85,7 @@ def lib() -> C.CDLL:
     L.nx_sim_error.argtypes = [C.c_void_p, C.c_int32, C.c_char_p, C.c_int64]
     L.nx_sim_rebuild_workloads.argtypes = [C.c_void_p, C.c_int32]
     L.nx_sim_summary_json.argtypes = [C.c_void_p, C.c_int32, C.c_char_p, C.c_int64, _P(C.c_int64)]
+    L.nx_sim_metrics.argtypes = [C.c_void_p, C.c_int32, _P(ReplicaMetrics)]
     L.nx_sim_records.argtypes = [C.c_void_p, C.c_int32, _P(RequestRecord), C.c_int64, _P(C.c_int64)]
     L.nx_sim_learner.argtypes = [C.c_void_p, C.c_int32, C.c_int32, _P(C.c_double), _P(C.c_int64),
                                  _P(C.c_int64)]

@@ -12,6 +12,7 @@
 #include <cstring>
 #include <filesystem>
 #include <fstream>
+#include <map>
 #include <memory>
 #include <numeric>
 #include <stdexcept>
@@ -32,6 +33,7 @@ extern "C" cudaError_t nx_launch_sim(const NxPools* d_pools, const int32_t* d_or
                                      int* d_next, int prefix_cap, int max_eng, int n_ew, int fsm_cap,
                                      int req_cap, size_t smem, int grid, cudaStream_t st);
 extern "C" size_t nx_sim_fit_table_doubles(int fsm_cap);
+extern "C" cudaError_t nx_launch_summarize(const NxPools* d_pools, int n_rep, double* work, cudaStream_t st);
 extern "C" size_t nx_sim_req_smem_bytes(int req_cap);
 extern "C" cudaError_t nx_sim_set_debug(unsigned long long* dev_ptr);
 
@@ -245,7 +247,8 @@ struct nx_sim {
   NxPools* d_pools = nullptr;
   int32_t* d_order = nullptr;
   int* d_next = nullptr;
-  size_t off_rep = 0, off_eng = 0, off_rep_out = 0, off_eng_out = 0;
+  size_t off_rep = 0, off_eng = 0, off_rep_out = 0, off_eng_out = 0, off_metrics = 0, off_sum_work = 0;
+  NxReplicaMetrics* h_metrics = nullptr;
   size_t off_state_begin = 0, off_state_end = 0;  // zero-initialised state span
   size_t off_ff_begin = 0, off_ff_end = 0;        // 0xff-initialised span
   int64_t h2d_bytes = 0, d2h_bytes = 0;
@@ -258,7 +261,7 @@ struct nx_sim {
     for (void* p : {(void*)h_arr_us, (void*)h_arr_ms, (void*)h_req0,
                     (void*)h_session, (void*)h_rep_out, (void*)h_eng_out, (void*)h_records,
                     (void*)h_first_us, (void*)h_done_us, (void*)h_req_engine, (void*)h_plan_log,
-                    (void*)h_route_log, (void*)h_learn_log})
+                    (void*)h_route_log, (void*)h_learn_log, (void*)h_metrics})
       if (p) cudaFreeHost(p);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
@@ -465,6 +468,8 @@ void fill_descriptors(nx_sim& h) {
   const size_t o_rlog = A.take<NxRouteLog>(h.n_route_log);
   const size_t o_llog = A.take<NxLearnLog>(h.n_learn_log);
   h.off_rep_out = A.take<NxReplicaOut>(h.n_rep);
+  h.off_metrics = A.take<NxReplicaMetrics>(h.n_rep);
+  h.off_sum_work = A.take<double>(4 * h.n_req);  // summary.cu: e2e, ttft, tpot, compacted tpot
   h.off_eng_out = A.take<NxEngineOut>(h.n_eng);
   h.arena_bytes = A.size;
 
@@ -518,6 +523,7 @@ void fill_descriptors(nx_sim& h) {
   P.eng = reinterpret_cast<const NxEngineDesc*>(B + h.off_eng);
   P.rep_out = reinterpret_cast<NxReplicaOut*>(B + h.off_rep_out);
   P.eng_out = reinterpret_cast<NxEngineOut*>(B + h.off_eng_out);
+  P.metrics = reinterpret_cast<NxReplicaMetrics*>(B + h.off_metrics);
   h.d_order = reinterpret_cast<int32_t*>(B + o_order);
   h.d_next = reinterpret_cast<int*>(B + o_next);
   cuda_check(cudaMalloc(&h.d_pools, sizeof(NxPools)), "cudaMalloc(pools)");
@@ -550,6 +556,7 @@ void fill_descriptors(nx_sim& h) {
   }
   std::stable_sort(h.order.begin(), h.order.end(), [&](int a, int b) { return cost[a] > cost[b]; });
   h.h_rep_out = pinned<NxReplicaOut>(h.n_rep);
+  h.h_metrics = pinned<NxReplicaMetrics>(h.n_rep);
   h.h_eng_out = pinned<NxEngineOut>(h.n_eng);
   h.h_records = pinned<int32_t>(h.n_req);
   h.h_first_us = pinned<int64_t>(h.n_req);
@@ -800,6 +807,9 @@ int nx_sim_launch(nx_sim_t h) {
     arm_debug_dump();
     cuda_check(nx_launch_sim(h->d_pools, h->d_order, h->n_rep, h->d_next, h->prefix_cap, h->max_eng, h->n_ew,
                              fsm_cap, req_cap, smem, grid, st), "nx_sim_kernel launch");
+    // K7: the metrics summaries on the device, same stream (summary.cu)
+    cuda_check(nx_launch_summarize(h->d_pools, h->n_rep, reinterpret_cast<double*>(h->d_arena + h->off_sum_work), st),
+               "nx_summarize_kernel launch");
     cuda_check(cudaEventRecord(h->ev1, st), "event");
     h->launched = true;
   });
@@ -815,6 +825,7 @@ int nx_sim_download(nx_sim_t h) {
     h->d2h_bytes = 0;
     const NxPools& P = h->pools;
     cp(h->h_rep_out, P.rep_out, h->n_rep * sizeof(NxReplicaOut));
+    cp(h->h_metrics, P.metrics, h->n_rep * sizeof(NxReplicaMetrics));
     cp(h->h_eng_out, P.eng_out, h->n_eng * sizeof(NxEngineOut));
     cp(h->h_records, P.records, h->n_req * sizeof(int32_t));
     cp(h->h_first_us, P.first_us, h->n_req * sizeof(int64_t));
@@ -919,6 +930,49 @@ int nx_sim_records(nx_sim_t h, int32_t replica, nx_request_record* out, int64_t 
   });
 }
 
+namespace {
+// The device's summary (summary.cu) as the report's Metrics: engine counts by
+// index become shares ordered by engine id (std::map in metrics.cpp:60-88).
+nx::Metrics device_metrics(const nx_sim& h, int32_t replica) {
+  const NxReplicaMetrics& dm = h.h_metrics[replica];
+  const NxReplicaDesc& d = h.rep[replica];
+  if (!dm.valid) throw std::invalid_argument("RequestRecord timestamps out of order");
+  nx::Metrics m;
+  m.completed = dm.completed;
+  if (dm.completed == 0) return m;
+  m.p50_e2e = dm.p50_e2e;
+  m.p90_e2e = dm.p90_e2e;
+  m.p50_ttft = dm.p50_ttft;
+  m.p50_tpot = dm.p50_tpot;
+  m.mean_ttft = dm.mean_ttft;
+  m.mean_tpot = dm.mean_tpot;
+  m.slo_pct = dm.slo_pct;
+  std::map<int, int64_t> per_engine;
+  for (int e = 0; e < d.n_eng; ++e)
+    if (dm.engine_count[e]) per_engine[h.eng[d.eng_base + e].engine_id] += dm.engine_count[e];
+  for (const auto& [id, cnt] : per_engine)
+    m.engine_share.emplace_back(id, static_cast<double>(cnt) / static_cast<double>(dm.completed));
+  return m;
+}
+}  // namespace
+
+extern "C" int nx_sim_metrics(nx_sim_t h, int32_t replica, nx_replica_metrics* out) {
+  return guard([&] {
+    if (replica < 0 || replica >= h->n_rep) throw std::invalid_argument("replica out of range");
+    const NxReplicaOut& o = h->h_rep_out[replica];
+    if (o.status != 0) throw std::runtime_error(replica_message(o));
+    const nx::Metrics m = device_metrics(*h, replica);
+    out->completed = m.completed;
+    out->p50_e2e_ms = m.p50_e2e;
+    out->p90_e2e_ms = m.p90_e2e;
+    out->p50_ttft_ms = m.p50_ttft;
+    out->p50_tpot_ms = m.p50_tpot;
+    out->mean_ttft_ms = m.mean_ttft;
+    out->mean_tpot_ms = m.mean_tpot;
+    out->slo_attainment_pct = m.slo_pct;
+  });
+}
+
 int nx_sim_summary_json(nx_sim_t h, int32_t replica, char* buf, int64_t cap, int64_t* len) {
   return guard([&] {
     if (replica < 0 || replica >= h->n_rep) throw std::invalid_argument("replica out of range");
@@ -930,27 +984,13 @@ int nx_sim_summary_json(nx_sim_t h, int32_t replica, char* buf, int64_t cap, int
       throw std::runtime_error(msg);
     }
     const NxReplicaDesc& d = h->rep[replica];
-    std::vector<nx_request_record> recs(static_cast<size_t>(o.completed));
-    int64_t n = 0;
-    if (nx_sim_records(h, replica, recs.data(), o.completed, &n) != NX_OK)
-      throw std::runtime_error(g_err);
-    std::vector<nx::RecordRow> rows(recs.size());
-    for (size_t i = 0; i < recs.size(); ++i) {
-      rows[i].request_id = recs[i].request_id;
-      rows[i].arrival_ms = recs[i].arrival_ms;
-      rows[i].first_token_ms = recs[i].first_token_ms;
-      rows[i].completed_ms = recs[i].completed_ms;
-      rows[i].prompt_tokens = recs[i].prompt_tokens;
-      rows[i].output_tokens = recs[i].output_tokens;
-      rows[i].engine_id = recs[i].engine_id;
-    }
     const nx::RunCfg& c = h->cfgs[replica];
     std::vector<nx::LearnerRow> learners;
     for (int e = 0; e < d.n_eng; ++e) {
       const NxEngineOut& eo = h->h_eng_out[d.eng_base + e];
       learners.push_back({h->eng[d.eng_base + e].engine_id, eo.samples, eo.params[5]});
     }
-    const nx::Metrics m = nx::summarize_records(rows, c.ttft_slo, c.tpot_slo);
+    const nx::Metrics m = device_metrics(*h, replica);
     const std::string s = nx::build_summary_json(
         c, o.arrived, o.completed, o.rejected, o.arrived - o.rejected - o.completed + o.pending,
         h->wl[replica].arrival_hash, o.event_hash, m, learners);

@@ -92,6 +92,16 @@ typedef struct NxReplicaOut {
   int64_t n_plan_log, n_route_log, n_learn_log;  /* rows written to the logs */
 } NxReplicaOut;
 
+/* Per-replica metrics summary computed on the device (device/summary.cu):
+   servesim::MetricsSummary (metrics.h) with engine counts by engine index. */
+typedef struct NxReplicaMetrics {
+  double p50_e2e, p90_e2e, p50_ttft, p50_tpot, mean_ttft, mean_tpot, slo_pct;
+  int64_t completed;
+  int32_t valid;           /* 0: a record's timestamps were out of order (metrics.cpp:13-16) */
+  int32_t n_tpot;          /* multi-token requests */
+  int32_t engine_count[NX_MAX_ENGINES];
+} NxReplicaMetrics;
+
 typedef struct NxEngineOut {
   double params[8];        /* learner's current PerfParams */
   int64_t samples;         /* OnlineLearner::samples_seen */
@@ -149,6 +159,7 @@ typedef struct NxPools {
   /* descriptors + outputs */
   const NxReplicaDesc* rep; const NxEngineDesc* eng;
   NxReplicaOut* rep_out; NxEngineOut* eng_out;
+  NxReplicaMetrics* metrics;   /* device-side summaries (summary.cu) */
 } NxPools;
 
 enum {

@@ -90,6 +90,12 @@ class Batch:
         check(lib().nx_sim_summaries(self.h, out))
         return list(out)
 
+    def metrics(self, r: int) -> dict:
+        """servesim::MetricsSummary of replica r, computed on the device (K7)."""
+        m = _lib.ReplicaMetrics()
+        check(lib().nx_sim_metrics(self.h, r, C.byref(m)))
+        return {k: getattr(m, k) for k, _ in m._fields_}
+
     def summary_json(self, r: int) -> str:
         n = C.c_int64()
         check(lib().nx_sim_summary_json(self.h, r, None, 0, C.byref(n)))

@@ -52,7 +52,7 @@ def all_cases(tmp_path_factory):
 
 @pytest.fixture(scope="module")
 def device_batch(all_cases):
-    """Every parity case as ONE device batch (one warp per replica)."""
+    """Every parity case as ONE device batch (one CTA per replica)."""
     from paper_2509_23384_b200 import sim
     names = sorted(all_cases)
     b = sim.Batch([all_cases[n] for n in names]).run()

@@ -374,6 +374,13 @@ def operators(torch, dev) -> dict:
     if (plans["status"] != 0).any():
         raise RuntimeError("nx_lens_schedule: problem errors")
     out["lens_decisions_per_s"] = n / t
+    # the same batch in NX_FAST_FP32 (float probes; decisions may differ)
+    t32 = timed(lambda: check(lib().nx_lens_schedule_mode_dev(dP.data_ptr(), n, dR.data_ptr(), rem.size,
+                                                              dPl.data_ptr(), dA.data_ptr(), 1,
+                                                              C.c_void_p(stream.cuda_stream))))
+    p32 = np.frombuffer(dPl.cpu().numpy().tobytes(), dtype=abi.LENS_PLAN)
+    out["lens_fp32_decisions_per_s"] = n / t32
+    out["lens_fp32_same_plan_frac"] = float(np.mean((p32["b"] == plans["b"]) & (p32["s"] == plans["s"])))
     out["lens_batch"] = f"{n} decisions, |run| U[0,64), |wait| U[0,64)"
     # K3: routers of 8 engines, 32 PRISM routes each (sequential within a group)
     g, e, m = 1 << 14, 8, 32

@@ -105,6 +105,19 @@ int nx_lens_schedule_dev(const nx_lens_problem* problems, int32_t n_problems,
 int nx_lens_schedule_host(const nx_lens_problem* problems, int32_t n_problems,
                           const int32_t* wait_remaining, int64_t n_wait_total,
                           nx_lens_plan* plans, int32_t* alloc_tokens);
+/* The same with an evaluation mode: NX_DETERMINISTIC_FP64 (the two calls
+ * above: bit-exact decisions) or NX_FAST_FP32 (every probe of the budget
+ * search and the candidate errors in float; predicted_ms within 1e-4
+ * relative of the fp64 model for the chosen plan; decisions can differ from
+ * the deterministic mode where two candidates, or a probe and the target,
+ * lie within float rounding of each other). Validation, the prefix and the
+ * allocation lists are the deterministic mode's. Any other mode: NX_EINVAL. */
+int nx_lens_schedule_mode_dev(const nx_lens_problem* problems, int32_t n_problems,
+                              const int32_t* wait_remaining, int64_t n_wait_total,
+                              nx_lens_plan* plans, int32_t* alloc_tokens, int32_t mode, void* stream);
+int nx_lens_schedule_mode_host(const nx_lens_problem* problems, int32_t n_problems,
+                               const int32_t* wait_remaining, int64_t n_wait_total,
+                               nx_lens_plan* plans, int32_t* alloc_tokens, int32_t mode);
 
 /* ---- K3: batched PRISM routing ---------------------------------------------
  * Replaces servesim::Router::route (proj/include/servesim/router.h:55-121,

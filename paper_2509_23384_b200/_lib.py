@@ -119,6 +119,8 @@ def lib() -> C.CDLL:
     L.nx_abi_sizes.argtypes = [_P(C.c_int64), C.c_int32]
     L.nx_lens_schedule_dev.argtypes = [V, C.c_int32, V, C.c_int64, V, V, V]
     L.nx_lens_schedule_host.argtypes = [V, C.c_int32, V, C.c_int64, V, V]
+    L.nx_lens_schedule_mode_dev.argtypes = [V, C.c_int32, V, C.c_int64, V, V, C.c_int32, V]
+    L.nx_lens_schedule_mode_host.argtypes = [V, C.c_int32, V, C.c_int64, V, V, C.c_int32]
     L.nx_baseline_schedule_host.argtypes = [V, C.c_int32, V, C.c_int64, V]
     L.nx_prism_route_dev.argtypes = [V, C.c_int32, V, V, V, V, V, V]
     L.nx_prism_route_host.argtypes = [V, C.c_int32, V, C.c_int64, V, C.c_int64, V, C.c_int64, V, V]

@@ -138,4 +138,99 @@ __device__ __forceinline__ LensPick lens_sweep(int lane, const Params& P, int R,
   return pick;
 }
 
+// ---- NX_FAST_FP32 (include/nx_sched.h) --------------------------------------
+// The same sweep with every probe in float: f_B, f_S, the predicted latency
+// and the error. Decisions follow the fp32 arithmetic (they can differ from
+// the deterministic mode where two candidates or a probe and the target lie
+// within float rounding of each other); predicted latencies are within 1e-4
+// relative of the fp64 model for the plan chosen. Used by the batched K2
+// entry point only; the simulator always runs the deterministic sweep.
+struct ParamsF {
+  float tau0, w0, ws, tauB, tauS, p_max, kB, kS;
+};
+__device__ __forceinline__ ParamsF params_f32(const Params& p) {
+  ParamsF f;
+  f.tau0 = static_cast<float>(p.tau0); f.w0 = static_cast<float>(p.w0); f.ws = static_cast<float>(p.ws);
+  f.tauB = static_cast<float>(p.tauB); f.tauS = static_cast<float>(p.tauS);
+  f.p_max = static_cast<float>(p.p_max); f.kB = static_cast<float>(p.kB); f.kS = static_cast<float>(p.kS);
+  return f;
+}
+__device__ __forceinline__ float sat_f32(float k, float x) {
+  return fminf(-expm1f(-k * x), 0x1.fffffep-1f);
+}
+__device__ __forceinline__ float latency_fb_f32(const ParamsF& p, float fb, float b, float s) {
+  const float thr = p.p_max * fb * sat_f32(p.kS, s);
+  return p.tau0 + (p.w0 + p.ws * s) / thr + p.tauB * b + p.tauS * s;
+}
+
+__device__ __forceinline__ LensPick lens_sweep_f32(int lane, const Params& P64, int R, int span, int mmax,
+                                                   int iters, double target64, double eps_ratio,
+                                                   const int32_t* pre) {
+  const ParamsF P = params_f32(P64);
+  const float target = static_cast<float>(target64);
+  const int b_lo = R > 1 ? R : 1;
+  const int b_hi = R + span;
+  const float thr_eps = static_cast<float>(target64 * eps_ratio);
+  float best_err = __builtin_huge_valf(), best_T = 0.0f;
+  int best_budget = -1;
+  for (int B0 = b_lo; B0 <= b_hi; B0 += 32) {
+    const int B = B0 + lane;
+    const bool act = B <= b_hi;
+    float err = __builtin_huge_valf(), T = 0.0f;
+    int budget = 0;
+    if (act) {
+      const int avail = R + pre[B - R];
+      int s_cap = (mmax < avail) ? mmax : avail;
+      s_cap = (B < s_cap) ? s_cap : B;
+      const float bd = static_cast<float>(B);
+      const float fb = sat_f32(P.kB, bd);
+      int lo = B, hi = s_cap;
+      budget = B;
+      for (int it = 0; it < iters; ++it) {
+        if (lo > hi) break;
+        const int mid = lo + (hi - lo) / 2;
+        if (latency_fb_f32(P, fb, bd, static_cast<float>(mid)) <= target) {
+          budget = mid;
+          lo = mid + 1;
+        } else {
+          hi = mid - 1;
+        }
+      }
+      const int j = lens_lower_bound(pre, B - R, budget - R);
+      const float bj = static_cast<float>(R + j);
+      T = latency_fb_f32(P, sat_f32(P.kB, bj), bj, static_cast<float>(budget));
+      err = fabsf(T - target);
+    }
+    const unsigned hit = __ballot_sync(NX_FULL, act && err < thr_eps);
+    if (hit) {
+      best_budget = __shfl_sync(NX_FULL, budget, __ffs(hit) - 1);
+      best_T = __shfl_sync(NX_FULL, T, __ffs(hit) - 1);
+      break;
+    }
+    float v = (act && !isnan(err)) ? err : __builtin_huge_valf();
+    int who = lane;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float ov = __shfl_xor_sync(NX_FULL, v, o);
+      const int ow = __shfl_xor_sync(NX_FULL, who, o);
+      if (ov < v || (ov == v && ow < who)) {
+        v = ov;
+        who = ow;
+      }
+    }
+    const int wb = __shfl_sync(NX_FULL, budget, who & 31);
+    const float wT = __shfl_sync(NX_FULL, T, who & 31);
+    if (v < best_err) {
+      best_err = v;
+      best_budget = wb;
+      best_T = wT;
+    }
+  }
+  LensPick pick;
+  pick.budget = best_budget;
+  pick.T = static_cast<double>(best_T);
+  pick.j = best_budget >= 0 ? lens_lower_bound(pre, span, best_budget - R) : 0;
+  return pick;
+}
+
 }  // namespace nxd

@@ -24,6 +24,9 @@ __device__ __forceinline__ bool lens_cfg_valid(const nx_lens_problem& p) {  // l
          p.eps_ratio < 1.0 && p.q_ref > 0.0;
 }
 
+// kF32: NX_FAST_FP32 (lens_sweep_f32); validation, prefix and allocation are
+// the deterministic mode's.
+template <bool kF32>
 __global__ void __launch_bounds__(32 * kLensWarps) nx_lens_kernel(
     const nx_lens_problem* __restrict__ probs, int n_prob, const int32_t* __restrict__ rem,
     nx_lens_plan* __restrict__ plans, int32_t* __restrict__ alloc, int32_t* __restrict__ gpre) {
@@ -57,7 +60,13 @@ __global__ void __launch_bounds__(32 * kLensWarps) nx_lens_kernel(
       if (R > qmax) {  // transient overload (lens.cpp:107-117)
         out.b = qmax;
         out.s = qmax;
-        out.predicted_ms = predict(P, qmax, qmax);
+        if constexpr (kF32) {
+          const ParamsF F = params_f32(P);
+          const float q = static_cast<float>(qmax);
+          out.predicted_ms = latency_fb_f32(F, sat_f32(F.kB, q), q, q);
+        } else {
+          out.predicted_ms = predict(P, qmax, qmax);
+        }
         out.overload = 1;
         out.n_decode = qmax;
       } else if (!(target > 0.0)) {
@@ -91,8 +100,9 @@ __global__ void __launch_bounds__(32 * kLensWarps) nx_lens_kernel(
         if (__any_sync(NX_FULL, bad)) {
           out.status = NX_EINVAL;
         } else {
-          const LensPick pick = lens_sweep(lane, P, R, span, mmax, pr.n_search_iters, target,
-                                           pr.eps_ratio, pre);
+          const LensPick pick =
+              kF32 ? lens_sweep_f32(lane, P, R, span, mmax, pr.n_search_iters, target, pr.eps_ratio, pre)
+                   : lens_sweep(lane, P, R, span, mmax, pr.n_search_iters, target, pr.eps_ratio, pre);
           if (pick.budget < 0) {  // every error NaN: the default (empty) BatchPlan
             out.target_ms = 0.0;
           } else {
@@ -394,13 +404,14 @@ extern "C" int64_t nx_refit_scratch_per(int64_t W) {
 
 extern "C" cudaError_t nx_launch_lens(const nx_lens_problem* probs, int n, const int32_t* rem,
                                       nx_lens_plan* plans, int32_t* alloc, int32_t* gpre, int sms,
-                                      cudaStream_t st) {
+                                      int mode, cudaStream_t st) {
   using namespace nxd;
   int grid = (n + kLensWarps - 1) / kLensWarps;
   const int cap = sms * 8;
   if (grid > cap) grid = cap;
   if (grid < 1) grid = 1;
-  nx_lens_kernel<<<grid, 32 * kLensWarps, 0, st>>>(probs, n, rem, plans, alloc, gpre);
+  if (mode == NX_FAST_FP32) nx_lens_kernel<true><<<grid, 32 * kLensWarps, 0, st>>>(probs, n, rem, plans, alloc, gpre);
+  else nx_lens_kernel<false><<<grid, 32 * kLensWarps, 0, st>>>(probs, n, rem, plans, alloc, gpre);
   return cudaGetLastError();
 }
 

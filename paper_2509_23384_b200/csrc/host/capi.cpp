@@ -75,7 +75,7 @@ extern "C" cudaError_t nx_launch_perf_eval(const double* params, int n_params, c
 
 extern "C" cudaError_t nx_launch_lens(const nx_lens_problem* probs, int n, const int32_t* rem,
                                       nx_lens_plan* plans, int32_t* alloc, int32_t* gpre, int sms,
-                                      cudaStream_t st);
+                                      int mode, cudaStream_t st);
 extern "C" cudaError_t nx_launch_route(nx_route_group* groups, int n, nx_engine_report* reports,
                                        const nx_route_request* reqs, int32_t* smap,
                                        nx_route_decision* dec, int32_t* gstatus, int sms,
@@ -1249,11 +1249,12 @@ int nx_abi_sizes(int64_t* out, int32_t n) {
   return NX_OK;
 }
 
-int nx_lens_schedule_dev(const nx_lens_problem* problems, int32_t n_problems,
-                         const int32_t* wait_remaining, int64_t n_wait_total, nx_lens_plan* plans,
-                         int32_t* alloc_tokens, void* stream) {
+int nx_lens_schedule_mode_dev(const nx_lens_problem* problems, int32_t n_problems,
+                              const int32_t* wait_remaining, int64_t n_wait_total, nx_lens_plan* plans,
+                              int32_t* alloc_tokens, int32_t mode, void* stream) {
   return guard([&] {
     if (n_problems < 0 || n_wait_total < 0) throw std::invalid_argument("nx_lens_schedule: negative sizes");
+    if (mode != NX_DETERMINISTIC_FP64 && mode != NX_FAST_FP32) throw std::invalid_argument("nx_lens_schedule: unknown mode");
     if (n_problems == 0) return;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     retain_default_pool();
@@ -1262,16 +1263,23 @@ int nx_lens_schedule_dev(const nx_lens_problem* problems, int32_t n_problems,
                                sizeof(int32_t) * static_cast<size_t>(n_wait_total + n_problems), st),
                "cudaMallocAsync");
     cudaError_t e = nx_launch_lens(problems, n_problems, wait_remaining, plans, alloc_tokens, gpre,
-                                   current_sms(), st);
+                                   current_sms(), mode, st);
     const cudaError_t e2 = cudaFreeAsync(gpre, st);
     cuda_check(e, "nx_lens_kernel launch");
     cuda_check(e2, "cudaFreeAsync");
   });
 }
 
-int nx_lens_schedule_host(const nx_lens_problem* problems, int32_t n_problems,
-                          const int32_t* wait_remaining, int64_t n_wait_total, nx_lens_plan* plans,
-                          int32_t* alloc_tokens) {
+int nx_lens_schedule_dev(const nx_lens_problem* problems, int32_t n_problems,
+                         const int32_t* wait_remaining, int64_t n_wait_total, nx_lens_plan* plans,
+                         int32_t* alloc_tokens, void* stream) {
+  return nx_lens_schedule_mode_dev(problems, n_problems, wait_remaining, n_wait_total, plans, alloc_tokens,
+                                   NX_DETERMINISTIC_FP64, stream);
+}
+
+int nx_lens_schedule_mode_host(const nx_lens_problem* problems, int32_t n_problems,
+                               const int32_t* wait_remaining, int64_t n_wait_total, nx_lens_plan* plans,
+                               int32_t* alloc_tokens, int32_t mode) {
   return guard([&] {
     if (n_problems < 0 || n_wait_total < 0) throw std::invalid_argument("nx_lens_schedule: negative sizes");
     if (n_problems == 0) return;
@@ -1286,8 +1294,8 @@ int nx_lens_schedule_host(const nx_lens_problem* problems, int32_t n_problems,
     cuda_check(cudaMemcpy(S.at<void>(op), problems, sizeof(nx_lens_problem) * n_problems, cudaMemcpyHostToDevice), "H2D");
     if (n_wait_total)
       cuda_check(cudaMemcpy(S.at<void>(orm), wait_remaining, sizeof(int32_t) * n_wait_total, cudaMemcpyHostToDevice), "H2D");
-    const int rc = nx_lens_schedule_dev(S.at<nx_lens_problem>(op), n_problems, S.at<int32_t>(orm),
-                                        n_wait_total, S.at<nx_lens_plan>(opl), S.at<int32_t>(oal), nullptr);
+    const int rc = nx_lens_schedule_mode_dev(S.at<nx_lens_problem>(op), n_problems, S.at<int32_t>(orm), n_wait_total,
+                                             S.at<nx_lens_plan>(opl), S.at<int32_t>(oal), mode, nullptr);
     if (rc) throw NxError(rc, g_err);
     cuda_check(cudaMemcpy(plans, S.at<void>(opl), sizeof(nx_lens_plan) * n_problems, cudaMemcpyDeviceToHost), "D2H");
     if (n_wait_total)
@@ -1297,6 +1305,13 @@ int nx_lens_schedule_host(const nx_lens_problem* problems, int32_t n_problems,
         throw NxError(plans[i].status, "schedule_step: problem " + std::to_string(i) + ": " +
                                            status_text(plans[i].status));
   });
+}
+
+int nx_lens_schedule_host(const nx_lens_problem* problems, int32_t n_problems,
+                          const int32_t* wait_remaining, int64_t n_wait_total, nx_lens_plan* plans,
+                          int32_t* alloc_tokens) {
+  return nx_lens_schedule_mode_host(problems, n_problems, wait_remaining, n_wait_total, plans, alloc_tokens,
+                                    NX_DETERMINISTIC_FP64);
 }
 
 int nx_prism_route_dev(nx_route_group* groups, int32_t n_groups, nx_engine_report* reports,

@@ -14,7 +14,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import abi
-from ._lib import check, lib
+from ._lib import NX_DETERMINISTIC_FP64, NX_FAST_FP32, check, lib  # noqa: F401 (mode constants re-exported)
 from .perf_model import PerfParams, _row
 
 
@@ -89,33 +89,36 @@ def problem_record(n_run: int, n_wait: int, wait_off: int, slo: SLOSpec, tm: Tra
     return r
 
 
-def schedule_batch(problems: np.ndarray, wait_remaining: np.ndarray, raise_errors: bool = True):
+def schedule_batch(problems: np.ndarray, wait_remaining: np.ndarray, raise_errors: bool = True,
+                   mode: int = NX_DETERMINISTIC_FP64):
     """Batched schedule_step on host arrays (copies in/out included).
 
     problems: nx_lens_problem records; wait_remaining: int32 remaining
     prompts, CSR by problems["wait_off"/"n_wait"]. Returns (plans,
     alloc_tokens) — plans are nx_lens_plan records; alloc_tokens[wait_off+k]
     holds waiter k's prefill chunk for k < n_prefill. With raise_errors
-    False, failing problems only report their status in the plan.
+    False, failing problems only report their status in the plan. mode:
+    NX_DETERMINISTIC_FP64 (bit-exact) or NX_FAST_FP32 (float probes).
     """
     problems = np.ascontiguousarray(problems, dtype=abi.LENS_PROBLEM)
     rem = np.ascontiguousarray(wait_remaining, dtype=np.int32)
     plans = np.zeros(problems.size, dtype=abi.LENS_PLAN)
     alloc = np.zeros(rem.size, dtype=np.int32)
-    rc = lib().nx_lens_schedule_host(abi.ptr(problems), problems.size, abi.ptr(rem), rem.size,
-                                     abi.ptr(plans), abi.ptr(alloc))
+    rc = lib().nx_lens_schedule_mode_host(abi.ptr(problems), problems.size, abi.ptr(rem), rem.size,
+                                          abi.ptr(plans), abi.ptr(alloc), mode)
     if raise_errors or not (plans["status"] != 0).any():
         check(rc)  # per-problem failures leave every plan written (status field)
     return plans, alloc
 
 
-def schedule_batch_device(problems, wait_remaining, plans, alloc_tokens, stream=None):
+def schedule_batch_device(problems, wait_remaining, plans, alloc_tokens, stream=None,
+                          mode: int = NX_DETERMINISTIC_FP64):
     """Stream-ordered batched schedule_step on torch CUDA tensors (uint8
     views of the record arrays for problems/plans, int32 for the waiters)."""
     st = stream.cuda_stream if stream is not None else None
-    check(lib().nx_lens_schedule_dev(problems.data_ptr(), problems.numel() // abi.LENS_PROBLEM.itemsize,
-                                     wait_remaining.data_ptr(), wait_remaining.numel(),
-                                     plans.data_ptr(), alloc_tokens.data_ptr(), st))
+    check(lib().nx_lens_schedule_mode_dev(problems.data_ptr(), problems.numel() // abi.LENS_PROBLEM.itemsize,
+                                          wait_remaining.data_ptr(), wait_remaining.numel(),
+                                          plans.data_ptr(), alloc_tokens.data_ptr(), mode, st))
 
 
 # ---- baseline engine policies (engine.h:68-79) -------------------------------------

@@ -130,6 +130,41 @@ def test_lens_plans_respect_feasibility_invariants(lens_run):
             assert p["n_decode"] == c["n_run"]
 
 
+def test_lens_fast_fp32_mode(lens_run):
+    """NX_FAST_FP32 (include/nx_sched.h): same validation and statuses, every
+    plan feasible, predicted_ms within 1e-4 of the fp64 model for the plan
+    it chose, and the same (b, s) as the deterministic mode on nearly every
+    decision (they may differ only where float rounding reorders two
+    candidates or a probe and the target; SURVEY App. A.5 validates the fast
+    mode statistically)."""
+    cases, probs, plans64, _ = lens_run
+    rem = []
+    for c in cases:
+        rem += [p - f for p, f in zip(c["prompt"], c["prefilled"])]
+    rem = np.asarray(rem, dtype=np.int32)
+    plans, alloc = lens.schedule_batch(probs, rem, raise_errors=False, mode=lens.NX_FAST_FP32)
+    same = valid = 0
+    for i, c in enumerate(cases):
+        p, q = plans[i], plans64[i]
+        assert int(p["status"]) == int(q["status"]), i
+        if p["status"] or (c["n_run"] == 0 and not c["prompt"]):
+            continue
+        valid += 1
+        assert p["b"] <= c["q_max"] and p["s"] <= c["m_max"]
+        assert p["b"] == p["n_decode"] + p["n_prefill"]
+        off = int(probs[i]["wait_off"])
+        toks = [int(alloc[off + k]) for k in range(int(p["n_prefill"]))]
+        assert all(1 <= t <= r for t, r in zip(toks, rem[off:off + len(toks)]))
+        assert int(p["n_decode"]) + sum(toks) == p["s"]
+        assert _close(p["target_ms"], q["target_ms"], 0.0)  # target stays fp64
+        want = ops_cases._predict(list(probs[i]["params"]), int(p["b"]), int(p["s"]))
+        assert _close(p["predicted_ms"], want, 1e-4), (i, float(p["predicted_ms"]), want)
+        same += (int(p["b"]), int(p["s"])) == (int(q["b"]), int(q["s"]))
+    assert valid > 400 and same >= 0.95 * valid, (same, valid)
+    with pytest.raises(ValueError):
+        lens.schedule_batch(probs[:1], rem, mode=7)
+
+
 def test_lens_scalar_api_mirrors_reference():
     R = [lens.Request(id=i, prompt_len=64, prefilled=64) for i in range(4)]
     W = [lens.Request(id=10 + i, prompt_len=p) for i, p in enumerate([100, 300, 5, 2000])]

@@ -414,6 +414,10 @@ def operators(torch, dev) -> dict:
     if int((dSt != 0).sum().item()):
         raise RuntimeError("nx_prism_route: group errors")
     out["prism_routes_per_s"] = g * m / t
+    t32 = timed(lambda: check(lib().nx_prism_route_mode_dev(dG.data_ptr(), g, dRp.data_ptr(), dQ.data_ptr(),
+                                                            dS.data_ptr(), dD.data_ptr(), dSt.data_ptr(), 1,
+                                                            C.c_void_p(stream.cuda_stream))))
+    out["prism_fp32_routes_per_s"] = g * m / t32
     out["prism_batch"] = f"{g} routers x {m} sequential routes, {e} engines each"
     # K4: structural refits on 4096-sample windows
     nr, wl = 1024, 4096

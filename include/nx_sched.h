@@ -176,6 +176,19 @@ int nx_prism_route_host(nx_route_group* groups, int32_t n_groups, nx_engine_repo
                         int64_t n_reports, const nx_route_request* requests, int64_t n_requests,
                         int32_t* session_map, int64_t n_session_entries,
                         nx_route_decision* decisions, int32_t* group_status);
+/* The same with an evaluation mode: NX_DETERMINISTIC_FP64 (the two calls
+ * above: bit-exact choices) or NX_FAST_FP32 (the PRISM policy's scores,
+ * factors and load ratios in float; choices can differ from the
+ * deterministic mode where two engines' scores lie within float rounding;
+ * the other policies are unchanged). Any other mode: NX_EINVAL. */
+int nx_prism_route_mode_dev(nx_route_group* groups, int32_t n_groups, nx_engine_report* reports,
+                            const nx_route_request* requests, int32_t* session_map,
+                            nx_route_decision* decisions, int32_t* group_status, int32_t mode,
+                            void* stream);
+int nx_prism_route_mode_host(nx_route_group* groups, int32_t n_groups, nx_engine_report* reports,
+                             int64_t n_reports, const nx_route_request* requests, int64_t n_requests,
+                             int32_t* session_map, int64_t n_session_entries,
+                             nx_route_decision* decisions, int32_t* group_status, int32_t mode);
 
 /* ---- K4: batched learner refits ---------------------------------------------
  * Replaces OnlineLearner::update_linear / update_structural

@@ -124,6 +124,8 @@ def lib() -> C.CDLL:
     L.nx_baseline_schedule_host.argtypes = [V, C.c_int32, V, C.c_int64, V]
     L.nx_prism_route_dev.argtypes = [V, C.c_int32, V, V, V, V, V, V]
     L.nx_prism_route_host.argtypes = [V, C.c_int32, V, C.c_int64, V, C.c_int64, V, C.c_int64, V, V]
+    L.nx_prism_route_mode_dev.argtypes = [V, C.c_int32, V, V, V, V, V, C.c_int32, V]
+    L.nx_prism_route_mode_host.argtypes = [V, C.c_int32, V, C.c_int64, V, C.c_int64, V, C.c_int64, V, V, C.c_int32]
     L.nx_refit_dev.argtypes = [C.c_int32, V, C.c_int32, V, V, V, C.c_int64, V, V]
     L.nx_refit_host.argtypes = [C.c_int32, V, C.c_int32, V, V, V, C.c_int64, V]
     _lib = L

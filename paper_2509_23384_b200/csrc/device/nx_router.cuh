@@ -120,4 +120,80 @@ __device__ __forceinline__ PrismPick prism_choose(const RouterCfgD& cfg, const E
   return p;
 }
 
+// NX_FAST_FP32 (include/nx_sched.h): prism_choose with the per-engine score,
+// its factors and the load ratio in float (expf / powf), and the "better"
+// scan over the float scores. Choices can differ from the deterministic mode
+// where two engines' scores lie within float rounding; scores and factors are
+// within ~1e-6 relative of the fp64 ones. Batched K3 entry point only.
+__device__ __forceinline__ PrismPick prism_choose_f32(const RouterCfgD& cfg, const EngineView& v,
+                                                      double demand, double now, int n) {
+  float f[4] = {1.0f, 1.0f, 1.0f, 1.0f};
+  float rho = 0.0f, score = 0.0f;
+  bool fresh = false;
+  if (v.on) {
+    const float age = v.has_rep ? static_cast<float>(now - v.at) : __builtin_huge_valf();
+    const float stale = static_cast<float>(cfg.stale_limit), ttft = static_cast<float>(cfg.ttft_slo);
+    const float wl = static_cast<float>(v.wload), pm = static_cast<float>(v.pmax);
+    const float half = static_cast<float>(cfg.load_half);
+    if (v.has_rep && age <= stale) {
+      fresh = true;
+      const float knee = static_cast<float>(cfg.knee) * ttft;
+      const float lh = static_cast<float>(v.lhat);
+      if (lh <= knee) {
+        f[0] = 1.0f;
+      } else {
+        const float scale = cfg.scale_ms > 0.0 ? static_cast<float>(cfg.scale_ms) : 0.25f * ttft;
+        f[0] = expf(-(lh - knee) / scale);
+      }
+      f[1] = 1.0f / (1.0f + (wl / pm) / half);
+      const float r = static_cast<float>(v.mfree) / (static_cast<float>(cfg.headroom) * static_cast<float>(demand));
+      const float cl = (r < 0.0f) ? 0.0f : ((1.0f < r) ? 1.0f : r);
+      f[2] = cl * cl;
+      rho = wl / pm;
+    } else {
+      f[0] = 0.5f;
+      f[2] = 0.5f;
+      if (v.has_rep) {
+        rho = wl / pm;
+        const float blend = expf(-(age - stale) / stale);
+        f[1] = 1.0f + (1.0f / (1.0f + rho / half) - 1.0f) * blend;
+      }
+    }
+    f[3] = v.affine ? static_cast<float>(cfg.beta_aff) : 1.0f;
+    score = 1.0f;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float w = static_cast<float>(cfg.w[i]);
+      float term;
+      if (f[i] == 0.0f && w > 0.0f) term = 0.0f;
+      else if (w == 1.0f) term = f[i];
+      else if (w == 0.0f) term = 1.0f;
+      else term = powf(f[i], w);
+      score *= term;
+    }
+  }
+  float best_s = -1.0f, best_rho = __builtin_huge_valf();
+  int best = -1, best_id = -1;
+  for (int e = 0; e < n; ++e) {
+    const float s = __shfl_sync(NX_FULL, score, e);
+    const float r = __shfl_sync(NX_FULL, rho, e);
+    const int id = __shfl_sync(NX_FULL, v.id, e);
+    const bool better = s > best_s || (s == best_s && (r < best_rho || (r == best_rho && id < best_id)));
+    if (best < 0 || better) {
+      best_s = s;
+      best_rho = r;
+      best = e;
+      best_id = id;
+    }
+  }
+  PrismPick p;
+  p.who = best;
+  p.score = best_s;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) p.f[i] = __shfl_sync(NX_FULL, f[i], best);
+  p.degraded = !__any_sync(NX_FULL, fresh);
+  if (p.degraded) p.who = prism_least_loaded(v);
+  return p;
+}
+
 }  // namespace nxd

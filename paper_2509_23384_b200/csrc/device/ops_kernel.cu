@@ -134,6 +134,7 @@ __global__ void __launch_bounds__(32 * kLensWarps) nx_lens_kernel(
 constexpr int kRouteWarps = 4;
 constexpr int kSessionCapacity = 100000;  // Router::kSessionCapacity (router.h:107)
 
+template <bool kF32>  // NX_FAST_FP32: prism_choose_f32 for the PRISM policy
 __global__ void __launch_bounds__(32 * kRouteWarps) nx_route_kernel(
     nx_route_group* __restrict__ groups, int n_groups, nx_engine_report* __restrict__ reports,
     const nx_route_request* __restrict__ reqs, int32_t* __restrict__ smap,
@@ -252,7 +253,8 @@ __global__ void __launch_bounds__(32 * kRouteWarps) nx_route_kernel(
           const double dem = static_cast<double>(rq.prompt_len) + lbar;
           const double demand = (1.0 < dem) ? dem : 1.0;
           v.affine = v.on && se == lane;
-          const PrismPick pk = prism_choose(rc, v, demand, rq.now_ms, n);
+          const PrismPick pk = kF32 ? prism_choose_f32(rc, v, demand, rq.now_ms, n)
+                                    : prism_choose(rc, v, demand, rq.now_ms, n);
           chosen = pk.who;
           o.score = pk.score;
           for (int i = 0; i < 4; ++i) o.factors[i] = pk.f[i];
@@ -418,13 +420,14 @@ extern "C" cudaError_t nx_launch_lens(const nx_lens_problem* probs, int n, const
 extern "C" cudaError_t nx_launch_route(nx_route_group* groups, int n, nx_engine_report* reports,
                                        const nx_route_request* reqs, int32_t* smap,
                                        nx_route_decision* dec, int32_t* gstatus, int sms,
-                                       cudaStream_t st) {
+                                       int mode, cudaStream_t st) {
   using namespace nxd;
   int grid = (n + kRouteWarps - 1) / kRouteWarps;
   const int cap = sms * 16;
   if (grid > cap) grid = cap;
   if (grid < 1) grid = 1;
-  nx_route_kernel<<<grid, 32 * kRouteWarps, 0, st>>>(groups, n, reports, reqs, smap, dec, gstatus);
+  if (mode == NX_FAST_FP32) nx_route_kernel<true><<<grid, 32 * kRouteWarps, 0, st>>>(groups, n, reports, reqs, smap, dec, gstatus);
+  else nx_route_kernel<false><<<grid, 32 * kRouteWarps, 0, st>>>(groups, n, reports, reqs, smap, dec, gstatus);
   return cudaGetLastError();
 }
 

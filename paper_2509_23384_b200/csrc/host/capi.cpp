@@ -79,7 +79,7 @@ extern "C" cudaError_t nx_launch_lens(const nx_lens_problem* probs, int n, const
 extern "C" cudaError_t nx_launch_route(nx_route_group* groups, int n, nx_engine_report* reports,
                                        const nx_route_request* reqs, int32_t* smap,
                                        nx_route_decision* dec, int32_t* gstatus, int sms,
-                                       cudaStream_t st);
+                                       int mode, cudaStream_t st);
 extern "C" cudaError_t nx_launch_refit(int kind, const nx_refit_problem* probs, int n,
                                        const int32_t* sb, const int32_t* ss, const double* sy,
                                        nx_refit_result* out, double* scratch, int64_t scratch_per,
@@ -1314,22 +1314,31 @@ int nx_lens_schedule_host(const nx_lens_problem* problems, int32_t n_problems,
                                     NX_DETERMINISTIC_FP64);
 }
 
-int nx_prism_route_dev(nx_route_group* groups, int32_t n_groups, nx_engine_report* reports,
-                       const nx_route_request* requests, int32_t* session_map,
-                       nx_route_decision* decisions, int32_t* group_status, void* stream) {
+int nx_prism_route_mode_dev(nx_route_group* groups, int32_t n_groups, nx_engine_report* reports,
+                            const nx_route_request* requests, int32_t* session_map,
+                            nx_route_decision* decisions, int32_t* group_status, int32_t mode,
+                            void* stream) {
   return guard([&] {
     if (n_groups < 0) throw std::invalid_argument("nx_prism_route: negative sizes");
+    if (mode != NX_DETERMINISTIC_FP64 && mode != NX_FAST_FP32) throw std::invalid_argument("nx_prism_route: unknown mode");
     if (n_groups == 0) return;
     cuda_check(nx_launch_route(groups, n_groups, reports, requests, session_map, decisions, group_status,
-                               current_sms(), static_cast<cudaStream_t>(stream)),
+                               current_sms(), mode, static_cast<cudaStream_t>(stream)),
                "nx_route_kernel launch");
   });
 }
 
-int nx_prism_route_host(nx_route_group* groups, int32_t n_groups, nx_engine_report* reports,
-                        int64_t n_reports, const nx_route_request* requests, int64_t n_requests,
-                        int32_t* session_map, int64_t n_session_entries,
-                        nx_route_decision* decisions, int32_t* group_status) {
+int nx_prism_route_dev(nx_route_group* groups, int32_t n_groups, nx_engine_report* reports,
+                       const nx_route_request* requests, int32_t* session_map,
+                       nx_route_decision* decisions, int32_t* group_status, void* stream) {
+  return nx_prism_route_mode_dev(groups, n_groups, reports, requests, session_map, decisions, group_status,
+                                 NX_DETERMINISTIC_FP64, stream);
+}
+
+int nx_prism_route_mode_host(nx_route_group* groups, int32_t n_groups, nx_engine_report* reports,
+                             int64_t n_reports, const nx_route_request* requests, int64_t n_requests,
+                             int32_t* session_map, int64_t n_session_entries,
+                             nx_route_decision* decisions, int32_t* group_status, int32_t mode) {
   return guard([&] {
     if (n_groups < 0 || n_reports < 0 || n_requests < 0 || n_session_entries < 0)
       throw std::invalid_argument("nx_prism_route: negative sizes");
@@ -1356,9 +1365,9 @@ int nx_prism_route_host(nx_route_group* groups, int32_t n_groups, nx_engine_repo
     h2d(orp, reports, sizeof(nx_engine_report) * n_reports);
     h2d(orq, requests, sizeof(nx_route_request) * n_requests);
     h2d(osm, session_map, sizeof(int32_t) * n_session_entries);
-    const int rc = nx_prism_route_dev(S.at<nx_route_group>(og), n_groups, S.at<nx_engine_report>(orp),
-                                      S.at<nx_route_request>(orq), S.at<int32_t>(osm),
-                                      S.at<nx_route_decision>(odc), S.at<int32_t>(ost), nullptr);
+    const int rc = nx_prism_route_mode_dev(S.at<nx_route_group>(og), n_groups, S.at<nx_engine_report>(orp),
+                                           S.at<nx_route_request>(orq), S.at<int32_t>(osm),
+                                           S.at<nx_route_decision>(odc), S.at<int32_t>(ost), mode, nullptr);
     if (rc) throw NxError(rc, g_err);
     d2h(groups, og, sizeof(nx_route_group) * n_groups);
     d2h(reports, orp, sizeof(nx_engine_report) * n_reports);
@@ -1370,6 +1379,14 @@ int nx_prism_route_host(nx_route_group* groups, int32_t n_groups, nx_engine_repo
         throw NxError(group_status[i], "Router::route: group " + std::to_string(i) + ": " +
                                            status_text(group_status[i]));
   });
+}
+
+int nx_prism_route_host(nx_route_group* groups, int32_t n_groups, nx_engine_report* reports,
+                        int64_t n_reports, const nx_route_request* requests, int64_t n_requests,
+                        int32_t* session_map, int64_t n_session_entries,
+                        nx_route_decision* decisions, int32_t* group_status) {
+  return nx_prism_route_mode_host(groups, n_groups, reports, n_reports, requests, n_requests, session_map,
+                                  n_session_entries, decisions, group_status, NX_DETERMINISTIC_FP64);
 }
 
 int nx_refit_dev(int32_t kind, const nx_refit_problem* problems, int32_t n_problems,

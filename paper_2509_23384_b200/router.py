@@ -119,16 +119,18 @@ class Router:
 
 
 def route_batch(groups: np.ndarray, reports: np.ndarray, requests: np.ndarray,
-                session_map: np.ndarray, raise_errors: bool = True):
+                session_map: np.ndarray, raise_errors: bool = True, mode: int = 0):
     """Batched Router::route on host record arrays (updated in place like the
-    routers' own state). Returns (decisions, group_status)."""
+    routers' own state). Returns (decisions, group_status). mode:
+    NX_DETERMINISTIC_FP64 (0, bit-exact) or NX_FAST_FP32 (1, float PRISM
+    scores)."""
     for a in (groups, reports, requests, session_map):
         assert a.flags["C_CONTIGUOUS"]
     dec = np.zeros(requests.size, dtype=abi.ROUTE_DECISION)
     st = np.zeros(groups.size, dtype=np.int32)
-    rc = lib().nx_prism_route_host(abi.ptr(groups), groups.size, abi.ptr(reports), reports.size,
-                                   abi.ptr(requests), requests.size, abi.ptr(session_map),
-                                   session_map.size, abi.ptr(dec), abi.ptr(st))
+    rc = lib().nx_prism_route_mode_host(abi.ptr(groups), groups.size, abi.ptr(reports), reports.size,
+                                        abi.ptr(requests), requests.size, abi.ptr(session_map),
+                                        session_map.size, abi.ptr(dec), abi.ptr(st), mode)
     if raise_errors or not (st != 0).any():
         check(rc)
     return dec, st

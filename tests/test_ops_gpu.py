@@ -248,6 +248,41 @@ def test_route_batch_matches_reference_router():
             assert float(reps["w_load_tokens"][eo + e]) == _unhex(want["states5"][e][1]), (g, e)
 
 
+def test_route_fast_fp32_mode():
+    """NX_FAST_FP32 for K3: same statuses, and the deterministic mode's
+    choices on nearly every routing decision (they may differ only where two
+    engines' float scores tie or swap within rounding; a group's later routes
+    then see a different dispatch echo, so they are compared only up to its
+    first difference). Scores and factors within 1e-4 relative there (the
+    fast mode's bound; the stale-report blend 1 + (f - 1) b cancels when b is
+    near 1, which turns float rounding into ~1e-5)."""
+    cases = ops_cases.route_cases()
+    groups, reps, reqs, smap = _route_inputs(cases)
+    d64, s64 = router.route_batch(groups, reps, reqs, smap, raise_errors=False)
+    groups, reps, reqs, smap = _route_inputs(cases)
+    d32, s32 = router.route_batch(groups, reps, reqs, smap, raise_errors=False, mode=1)
+    assert (s32 == s64).all()
+    agree = total = groups_ok = n_groups = 0
+    for g, c in enumerate(cases):
+        if s64[g]:
+            continue
+        n_groups += 1
+        o, m = int(groups[g]["request_off"]), len(c["req_prompt"])
+        total += m
+        for k in range(o, o + m):
+            if d32["engine_id"][k] != d64["engine_id"][k]:
+                break
+            agree += 1
+            assert _close(d32["score"][k], d64["score"][k], 1e-4), (g, k)
+            for j in range(4):
+                assert _close(d32["factors"][k][j], d64["factors"][k][j], 1e-4), (g, k, j)
+        else:
+            groups_ok += 1
+    assert total > 1000 and agree >= 0.9 * total and groups_ok >= 0.9 * n_groups, (agree, total, groups_ok, n_groups)
+    with pytest.raises(ValueError):
+        router.route_batch(*_route_inputs(cases[:1]), mode=3)
+
+
 def test_route_errors_match_reference():
     c = ops_cases.route_cases()[0]
     groups, reps, reqs, smap = _route_inputs([c])

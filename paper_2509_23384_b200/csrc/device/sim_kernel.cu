@@ -1939,6 +1939,10 @@ extern "C" cudaError_t nx_launch_sim(const NxPools* d_pools, const int32_t* d_or
   cudaError_t err = cudaFuncSetAttribute(nx_sim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
   if (err != cudaSuccess) return err;
+  if (const char* cv = getenv("NX_CARVEOUT")) {  // shared-memory share of L1 (percent; A/B knob)
+    err = cudaFuncSetAttribute(nx_sim_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(cv));
+    if (err != cudaSuccess) return err;
+  }
   nx_sim_kernel<<<grid, 32 * (1 + n_ew), smem, st>>>(d_pools, d_order, n_rep, d_next, prefix_cap, max_eng, n_ew,
                                                       fsm_cap, req_cap);
   return cudaGetLastError();

@@ -789,12 +789,23 @@ int nx_sim_launch(nx_sim_t h) {
       req_cap = static_cast<int>(h->max_req);
     if (const char* v = std::getenv("NX_REQ_SMEM")) if (v[0] == '0') req_cap = 0;
     base += nx_sim_req_smem_bytes(req_cap);
-    if (room > base) {
-      const int64_t per = static_cast<int64_t>((room - base) / h->n_ew / sizeof(double)) -
-                          static_cast<int64_t>(nx_sim_fit_table_doubles(0));
-      if (per >= 256) fsm_cap = static_cast<int>(std::min<int64_t>(per, 4096));
+    // The fit tables stay in each warp's global scratch by default: every KB
+    // of shared memory comes out of the SM's L1, and the event loop's global
+    // accesses (queues, logs, request SoA) need it more than the refit's
+    // table reads need shared memory (bench shard: 30.4-30.8 vs 29.4-29.6 M
+    // decisions/s, 5 interleaved A/B pairs; profiles/r02_l1_ab.txt).
+    // NX_FIT_SMEM=auto: tables in the shared memory left over; =N: N entries.
+    if (const char* fc = std::getenv("NX_FIT_SMEM")) {
+      if (std::string(fc) == "auto") {
+        if (room > base) {
+          const int64_t per = static_cast<int64_t>((room - base) / h->n_ew / sizeof(double)) -
+                              static_cast<int64_t>(nx_sim_fit_table_doubles(0));
+          if (per >= 256) fsm_cap = static_cast<int>(std::min<int64_t>(per, 4096));
+        }
+      } else {
+        fsm_cap = std::atoi(fc) < 0 ? -1 : std::min(std::atoi(fc), 4096);
+      }
     }
-    if (const char* fc = std::getenv("NX_FIT_SMEM")) fsm_cap = std::atoi(fc) < 0 ? -1 : std::min(std::atoi(fc), 4096);
     const size_t smem = base + (fsm_cap >= 0 ? static_cast<size_t>(h->n_ew) * nx_sim_fit_table_doubles(fsm_cap) *
                                                    sizeof(double)
                                              : 0);

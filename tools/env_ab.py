@@ -6,7 +6,7 @@ import bench
 from paper_2509_23384_b200 import sim
 cfgs = bench.shard_configs(0, 512, 2000)
 base = dict(os.environ)
-for spec in sys.argv[1:] * 2:  # each setting twice, interleaved
+for spec in sys.argv[1:] * int(os.environ.get("AB_REPS", "2")):  # each setting AB_REPS times, interleaved
     os.environ.clear(); os.environ.update(base)
     for kv in filter(None, spec.split(",")):
         k, v = kv.split("=")

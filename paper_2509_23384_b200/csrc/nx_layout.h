@@ -9,7 +9,9 @@
 
 #define NX_MAX_ENGINES 32      /* one lane per engine in the warp-wide scans */
 #define NX_TW_CAP 200          /* TradeoffEstimator::kWindow, proj/include/servesim/lens.h:145 */
+#ifndef NX_EVLOG_CAP
 #define NX_EVLOG_CAP (1 << 15) /* event-log ring entries per engine (power of two) */
+#endif
 
 /* Per-engine static description + pool offsets (one per engine, all replicas). */
 typedef struct NxEngineDesc {

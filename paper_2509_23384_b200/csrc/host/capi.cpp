@@ -1293,6 +1293,7 @@ int nx_lens_schedule_mode_host(const nx_lens_problem* problems, int32_t n_proble
                                int32_t* alloc_tokens, int32_t mode) {
   return guard([&] {
     if (n_problems < 0 || n_wait_total < 0) throw std::invalid_argument("nx_lens_schedule: negative sizes");
+    if (mode != NX_DETERMINISTIC_FP64 && mode != NX_FAST_FP32) throw std::invalid_argument("nx_lens_schedule: unknown mode");
     if (n_problems == 0) return;
     for (int32_t i = 0; i < n_problems; ++i)
       if (problems[i].n_wait < 0 || problems[i].wait_off < 0 ||
@@ -1353,6 +1354,7 @@ int nx_prism_route_mode_host(nx_route_group* groups, int32_t n_groups, nx_engine
   return guard([&] {
     if (n_groups < 0 || n_reports < 0 || n_requests < 0 || n_session_entries < 0)
       throw std::invalid_argument("nx_prism_route: negative sizes");
+    if (mode != NX_DETERMINISTIC_FP64 && mode != NX_FAST_FP32) throw std::invalid_argument("nx_prism_route: unknown mode");
     if (n_groups == 0) return;
     for (int32_t i = 0; i < n_groups; ++i) {
       const nx_route_group& g = groups[i];

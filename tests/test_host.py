@@ -39,6 +39,20 @@ def test_no_cuda_device_fails_loudly():
         sim.run_simulation(W.config1(n=10))
 
 
+def test_unknown_evaluation_mode_is_invalid_argument_before_any_device_work():
+    # NX_DETERMINISTIC_FP64 / NX_FAST_FP32 only (include/nx_sched.h); checked on
+    # the host, so the error class is the same with or without a GPU.
+    import numpy as np
+    from paper_2509_23384_b200 import abi, lens, router
+    probs = np.zeros(1, dtype=abi.LENS_PROBLEM)
+    with pytest.raises(ValueError):
+        lens.schedule_batch(probs, np.zeros(0, dtype=np.int32), mode=7)
+    g = np.zeros(1, dtype=abi.ROUTE_GROUP)
+    with pytest.raises(ValueError):
+        router.route_batch(g, np.zeros(0, dtype=abi.ENGINE_REPORT), np.zeros(0, dtype=abi.ROUTE_REQUEST),
+                           np.zeros(0, dtype=np.int32), mode=3)
+
+
 @pytest.mark.parametrize("name", sorted(static_cases()))
 def test_host_workload_reproduces_reference_arrivals(name):
     h, n, _ = sim.workload_info(static_cases()[name])

@@ -4,7 +4,8 @@ fixtures it produced.
 
 Bit-exact: event_hash (every routing choice, batch composition, token budget
 and event time), arrival_hash, every RequestRecord, the TTFT/TPOT/e2e/SLO
-metrics and engine shares. Tolerance: the learners' reported p_max (1e-9
+metrics and engine shares. Tolerance: the learners' reported p_max (1e-10
+on the golden cases with at least 30% bit-identical, 1e-9 at full size
 relative; device libm and tree-order accumulation differ from glibc in the
 last bits) and K1 predictions (1e-9 fp64, 1e-4 fp32 fast mode).
 """
@@ -23,22 +24,28 @@ pytestmark = pytest.mark.gpu
 
 ROOT = Path(__file__).resolve().parents[1]
 GOLDEN = json.loads((ROOT / "tests" / "golden" / "cases.json").read_text())
-P_MAX_TOL = 1e-9
+P_MAX_TOL = 1e-9           # full-size BASELINE configs (test_configs_gpu.py)
+GOLDEN_P_MAX_TOL = 1e-10   # the 28 golden cases: largest observed 1.08e-11 (tools/hist_stats.py)
 
 
 def _checker():
     return Ref() if ref_available() else Port()
 
 
-def assert_same_summary(want_json: str, got_json: str):
+def assert_same_summary(want_json: str, got_json: str, tol: float = P_MAX_TOL):
+    """Every summary field equal except learners[].p_max (relative `tol`);
+    returns (learners whose p_max is bit-identical, learners)."""
     a, b = json.loads(want_json), json.loads(got_json)
     for k in ("seed", "router_policy", "engines", "arrived", "completed", "rejected",
               "unfinished", "arrival_hash", "event_hash", "metrics", "engine_share"):
         assert a[k] == b[k], (k, a[k], b[k])
     assert len(a["learners"]) == len(b["learners"])
+    same = 0
     for la, lb in zip(a["learners"], b["learners"]):
         assert la["engine_id"] == lb["engine_id"] and la["samples"] == lb["samples"]
-        assert abs(la["p_max"] - lb["p_max"]) <= P_MAX_TOL * abs(la["p_max"])
+        assert abs(la["p_max"] - lb["p_max"]) <= tol * abs(la["p_max"])
+        same += la["p_max"] == lb["p_max"]
+    return same, len(a["learners"])
 
 
 @pytest.fixture(scope="module")
@@ -63,13 +70,18 @@ def device_batch(all_cases):
 def test_every_case_bit_exact_against_golden(device_batch):
     names, b = device_batch
     sums = b.summaries()
+    same = total = 0
     for i, name in enumerate(names):
         want = GOLDEN[name]
         assert sums[i].status == 0, name
         assert f"{sums[i].event_hash:016x}" == want["event_hash"], name
         assert f"{sums[i].arrival_hash:016x}" == want["arrival_hash"], name
         assert sums[i].decisions == want["decisions"], name
-        assert_same_summary(want["summary_json"], b.summary_json(i))
+        s, t = assert_same_summary(want["summary_json"], b.summary_json(i), GOLDEN_P_MAX_TOL)
+        same += s
+        total += t
+    # drift guard: 70 of the 167 learners' p_max are bit-identical today
+    assert same >= 0.3 * total, (same, total)
 
 
 def test_records_identical_to_reference(device_batch, all_cases):

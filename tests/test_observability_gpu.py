@@ -4,10 +4,11 @@ against the reference simulator on the same config: output.dir files
 and RunResult::learner_history (sim.cpp:322-327).
 
 Exact: every integer field, every row count and order, summary.json and
-requests.csv bytes (p_max in summary.json within 1e-9 like the main
+requests.csv bytes (p_max in summary.json within 1e-10 like the golden
 parity suite). Tolerance: device-libm floats in the logs — predicted
 latencies 1e-12 relative; route factors (which read the reported learner
-p_max) 1e-9; every learner coefficient of every history snapshot 1e-8.
+p_max) 1e-11; every learner coefficient of every history snapshot 1e-9, with
+at least a quarter of them bit-identical.
 """
 import copy
 import json
@@ -62,19 +63,28 @@ def test_output_files_and_history_match_reference(name, tmp_path):
     a, b = json.loads((R / "summary.json").read_text()), json.loads((D / "summary.json").read_text())
     for la, lb in zip(a.pop("learners"), b.pop("learners")):
         assert la["engine_id"] == lb["engine_id"] and la["samples"] == lb["samples"]
-        assert _close(la["p_max"], lb["p_max"], 1e-9)
+        assert _close(la["p_max"], lb["p_max"], 1e-10)
     assert a == b
     _cmp_rows(_rows(R / "plans.jsonl"), _rows(D / "plans.jsonl"),
               {"engine_id", "b", "s", "sim_time"}, 1e-12)
-    # route factors read the engines' reported p_max, itself within 1e-9
+    # route factors read the engines' reported p_max (largest observed
+    # difference 2e-13, tools/hist_stats.py)
     _cmp_rows(_rows(R / "routing.jsonl"), _rows(D / "routing.jsonl"),
-              {"request_id", "chosen_engine", "sim_time"}, 1e-9)
+              {"request_id", "chosen_engine", "sim_time"}, 1e-11)
     hist = want["learner_history"]
     assert len(hist) == len(got.learner_history) > 0
+    same = total = 0
     for (e0, t0, n0, p0), (e1, t1, n1, p1) in zip(hist, got.learner_history):
         assert (e0, t0, n0) == (e1, t1, n1)
         # every coefficient of every snapshot, not just the summary's p_max:
-        # w0 = a / c out of the ridge-anchored 5x5 solve amplifies the libm /
-        # reduction-order ulps (observed 1.2e-9), so 1e-8 here
-        bad = [(i, x, y) for i, (x, y) in enumerate(zip(p0, p1)) if not _close(x, y, 1e-8)]
+        # w0 = a / c out of the ridge-anchored 5x5 solve amplifies the device
+        # libm ulps in the noise and f_B / f_S values (largest observed on
+        # these cases 1.07e-10, prefill_priority; tools/hist_stats.py), so 1e-9
+        bad = [(i, x, y) for i, (x, y) in enumerate(zip(p0, p1)) if not _close(x, y, 1e-9)]
         assert not bad, (e0, t0, n0, bad)
+        same += sum(x == y for x, y in zip(p0, p1))
+        total += len(p0)
+    # drift guard: a third to over half of all coefficients are bit-identical
+    # to the reference's (observed 33-58% per case); a systematic drift that
+    # stayed inside the tolerance would show up here first
+    assert same >= 0.25 * total, (same, total)

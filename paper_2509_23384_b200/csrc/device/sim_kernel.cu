@@ -54,7 +54,10 @@ constexpr uint32_t kRootPar = 0x80000000u, kSelfRoot = 0x40000000u, kSeqMask = 0
 enum { kEvArrival = 0, kEvStep = 1, kEvReport = 2, kEvLearn = 3, kEvDeliver = 4 };  // sim.cpp:32-38
 constexpr uint32_t kMetaPlan = 8u;   // log meta: the event started a step and staged a plan row
 constexpr int kMetaFinShift = 8;     // log meta: requests a step completion finished
-constexpr int kRing = 256;           // shared-memory log entries per engine (merger's view)
+#ifndef NX_SRING
+#define NX_SRING 256
+#endif
+constexpr int kRing = NX_SRING;      // shared-memory log entries per engine (merger's view)
 // Phase timer slots of the diagnostic build (-DNX_TIMERS, tools/pdes_report.py)
 enum {
   kTmMerge = 0, kTmRoute = 1, kTmPlan = 2, kTmComplete = 3, kTmReport = 4, kTmLinear = 5,

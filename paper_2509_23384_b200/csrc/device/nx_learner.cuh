@@ -1336,70 +1336,112 @@ static __device__ NX_COLD void update_structural(Ctx& c, int e) {
   const double shrink = 1.0 - 1e-3;
   double th0 = log(cur.kB), th1 = log(cur.kS);
   double st0 = 0.5, st1 = 0.5;
-  FitOut best = gauged_fit(c, S, cur, exp(th0), exp(th1));
-#ifdef NX_TRACE_FIT
-  const bool tr = g.seen == 1024;
-  if (tr && c.lane == 0) printf("REFIT e=%d n=%d init err %.17g base %.17g\n", e, n, best.err, base.err);
-#endif
-  if (!isfinite(best.err)) {
-    __syncwarp();
-    if (c.lane == 0) g.cnt[5] += 1;
-    __syncwarp();
-    return;
-  }
   const double kbs[3] = {0.05, 0.7, 8.0}, kss[3] = {0.002, 0.03, 0.4};
-  for (int a = 0; a < 3; ++a) {
-    for (int bq = 0; bq < 3; ++bq) {
-      const FitOut cand = gauged_fit(c, S, cur, kbs[a], kss[bq]);
-#ifdef NX_TRACE_FIT
-      if (tr && c.lane == 0)
-        printf("  grid kB %.17g kS %.17g err %.17g bound %.3g best %.17g\n", kbs[a], kss[bq], cand.err, cand.bound, best.err);
-#endif
-      if (isfinite(cand.err) && less_scaled(c, S, cand, best, shrink)) {
-        th0 = log(kbs[a]);
-        th1 = log(kss[bq]);
-        best = cand;
-      }
-    }
-  }
-  for (int sweep = 0; sweep < 50; ++sweep) {
-    bool improved = false;
-    for (int cdim = 0; cdim < 2; ++cdim) {
-      bool hit = false;
-      for (int dir = 0; dir < 2 && !hit; ++dir) {
+  // learner.cpp:389-430 as a candidate generator around ONE gauged_fit call
+  // site: the start point, the 3x3 grid seed, the coordinate sweeps (+1 then
+  // -1 per coordinate, step x1.6 on a hit, x0.5 otherwise, stop when a sweep
+  // misses with both steps < 1e-5, at most 50 sweeps) and the winner's exact
+  // refit. Written as nested loops the fit was inlined four times (~0.8 MB
+  // of the kernel's code); one copy halves the kernel (96 k -> 50 k SASS
+  // instructions) at equal speed (profiles/r02_l1_ab.txt).
+  enum { kPhStart, kPhGrid, kPhSweep, kPhExact };
+  int ph = kPhStart, gi = 0, sweep = 0, cdim = 0, dir = 0;
+  bool hit = false, improved = false;
+  double t0 = th0, t1 = th1;
+  FitOut best;
+#pragma unroll 1
+  while (true) {
+    double kB, kS;
+    if (ph == kPhSweep) {  // the next candidate that moves its coordinate
+#pragma unroll 1
+      while (true) {
+        if (sweep >= 50) {
+          ph = kPhExact;
+          break;
+        }
+        if (cdim == 2) {  // end of a sweep
+          const double smax = (st0 < st1) ? st1 : st0;
+          if (!improved && smax < 1e-5) {
+            ph = kPhExact;
+            break;
+          }
+          ++sweep;
+          cdim = 0;
+          dir = 0;
+          hit = false;
+          improved = false;
+          continue;
+        }
+        if (hit || dir == 2) {  // this coordinate is done
+          if (cdim == 0) st0 *= hit ? 1.6 : 0.5;
+          else st1 *= hit ? 1.6 : 0.5;
+          improved |= hit;
+          ++cdim;
+          dir = 0;
+          hit = false;
+          continue;
+        }
         const double sgn = dir == 0 ? 1.0 : -1.0;
-        double t0 = th0, t1 = th1;
+        t0 = th0;
+        t1 = th1;
         double& tc = cdim == 0 ? t0 : t1;
         const double v = tc + sgn * (cdim == 0 ? st0 : st1);
         tc = (v < lo) ? lo : ((hi < v) ? hi : v);
-        if (tc == (cdim == 0 ? th0 : th1)) continue;
-        const FitOut cand = gauged_fit(c, S, cur, exp(t0), exp(t1));
-#ifdef NX_TRACE_FIT
-        if (tr && c.lane == 0)
-          printf("  sweep %d c %d kB %.17g kS %.17g err %.17g bound %.3g best %.17g\n", sweep, cdim, exp(t0), exp(t1),
-                 cand.err, cand.bound, best.err);
-#endif
-        if (isfinite(cand.err) && less_scaled(c, S, cand, best, shrink)) {
+        if (tc == (cdim == 0 ? th0 : th1)) {
+          ++dir;
+          continue;
+        }
+        break;
+      }
+    }
+    if (ph == kPhStart) {
+      kB = exp(th0);
+      kS = exp(th1);
+    } else if (ph == kPhGrid) {
+      kB = kbs[gi / 3];
+      kS = kss[gi % 3];
+    } else if (ph == kPhSweep) {
+      kB = exp(t0);
+      kS = exp(t1);
+    } else {
+      kB = best.p.kB;
+      kS = best.p.kS;
+    }
+    const long long tx = nx_clock();
+    const FitOut cand = gauged_fit(c, S, cur, kB, kS, ph == kPhExact);
+    if (ph == kPhStart) {
+      best = cand;
+      if (!isfinite(best.err)) {
+        __syncwarp();
+        if (c.lane == 0) g.cnt[5] += 1;
+        __syncwarp();
+        return;
+      }
+      ph = kPhGrid;
+    } else if (ph == kPhExact) {
+      // the winner's coefficients from the reference's exact normal equations
+      if (c.lane == 0) count(c.rs->lcycles[14], nx_clock() - tx);
+      if (isfinite(cand.err)) best = cand;
+      else best.err = cand.err;  // the exact system is singular: the reference fails this fit too
+      break;
+    } else {
+      if (isfinite(cand.err) && less_scaled(c, S, cand, best, shrink)) {
+        best = cand;
+        if (ph == kPhGrid) {
+          th0 = log(kB);
+          th1 = log(kS);
+        } else {
           th0 = t0;
           th1 = t1;
-          best = cand;
           hit = true;
         }
       }
-      if (cdim == 0) st0 *= hit ? 1.6 : 0.5;
-      else st1 *= hit ? 1.6 : 0.5;
-      improved |= hit;
+      if (ph == kPhGrid) {
+        if (++gi == 9) ph = kPhSweep;
+      } else {
+        ++dir;
+      }
     }
-    const double smax = (st0 < st1) ? st1 : st0;
-    if (!improved && smax < 1e-5) break;
-  }
-  // the winner's coefficients from the reference's exact normal equations
-  {
-    const long long tx = nx_clock();
-    const FitOut ex = gauged_fit(c, S, cur, best.p.kB, best.p.kS, true);
-    if (c.lane == 0) count(c.rs->lcycles[14], nx_clock() - tx);
-    if (isfinite(ex.err)) best = ex;
-    else best.err = ex.err;  // the exact system is singular: the reference fails this fit too
   }
   // reject if invalid or worse than the current model (learner.cpp:432-435)
   bool worse;

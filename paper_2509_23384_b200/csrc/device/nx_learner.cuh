@@ -1226,12 +1226,17 @@ static __device__ NX_COLD FitOut finish_fit(Ctx& c, const Stage& S, const Params
   for (int q = 0; q < 5; ++q) x[q] = xk[0][q];
   // lambda = min(1e-7, sse(x) / max(y2, 1e-30))  (learner.cpp:84-85, cap 1e-7)
   const double den = (y2 < 1e-30) ? 1e-30 : y2;
-  // Certify sse(x) / den >= 1e-7 (=> lambda = cap) from a lower bound: the
-  // sum has non-negative terms, so 32 of them evaluated directly (one per
-  // lane, the reference's per-term formula) bound the left-fold total from
-  // below; the closed form backs it up, the exact fold decides the rest.
-  double lb;
-  {
+  // Certify sse(x) / den >= 1e-7 (=> lambda = cap): first by the closed
+  // form (four warp sums; it clears the threshold by more than its rounding
+  // bound in nearly every fit), else by a lower bound — the sum has
+  // non-negative terms, so 32 of them evaluated directly (one per lane, the
+  // reference's per-term formula) bound the left-fold total from below —
+  // and the exact fold decides the rest.
+  const double thr = 1e-7 * (1.0 + 8.0 * kU);
+  double sv = 0.0, sb = 0.0;
+  closed_sse(e, x, n, y2, sv, sb);
+  bool at_cap = (sv - sb) / den > thr;
+  if (!at_cap) {
     const int i = c.lane * (n / 32);
     double rr = 0.0;
     if (i < n) {
@@ -1247,12 +1252,11 @@ static __device__ NX_COLD FitOut finish_fit(Ctx& c, const Stage& S, const Params
       const double r = (y - pred) / y;
       rr = r * r;
     }
-    lb = warp_sum(rr) * (1.0 - 1e-6);
+    const double lb = warp_sum(rr) * (1.0 - 1e-6);
+    at_cap = lb / den > thr;
   }
-  double sv = 0.0, sb = 0.0;
-  if (!(lb / den > 1e-7 * (1.0 + 8.0 * kU))) closed_sse(e, x, n, y2, sv, sb);
   double lambda = 1e-7;
-  if (!(lb / den > 1e-7 * (1.0 + 8.0 * kU)) && !((sv - sb) / den > 1e-7 * (1.0 + 8.0 * kU))) {
+  if (!at_cap) {
     const double v = sse_x_exact(c, S, kB, kS, x) / den;
     lambda = (v < 1e-7) ? v : 1e-7;
   }

@@ -122,9 +122,13 @@ int guard(F&& f) {
 }
 
 int sm_count(int device) {
+  thread_local int cached_dev = -1, cached_n = 0;  // queried once per device (scalar calls)
+  if (device == cached_dev) return cached_n;
   int n = 0;
   cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device);
-  return n > 0 ? n : 148;
+  cached_dev = device;
+  cached_n = n > 0 ? n : 148;
+  return cached_n;
 }
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
@@ -1218,10 +1222,78 @@ int nx_perf_eval_dev(const double* params, int32_t n_params, const int32_t* idx,
   });
 }
 
+// Small host batches (the scalar drop-in calls: predict_latency,
+// throughput): one packed copy each way through a pinned per-thread buffer —
+// parameters, inputs and a zeroed status word in, status + outputs out —
+// instead of four pageable copies, a memset, a status read and one or two
+// result reads (8 API calls → 3 and one synchronize).
+constexpr int64_t kPackedEvalMax = 1 << 16;
+
+// Grow-only pinned host buffer per thread for the packed host-pointer calls.
+static unsigned char* pinned_stage(size_t bytes) {
+  struct Pinned {
+    unsigned char* p = nullptr;
+    size_t cap = 0;
+  };
+  thread_local Pinned h;
+  if (h.cap < bytes) {
+    if (h.p) cudaFreeHost(h.p);
+    h.p = nullptr;
+    h.cap = 0;
+    const size_t cap = std::max<size_t>(bytes, size_t(1) << 16);
+    cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&h.p), cap, cudaHostAllocDefault), "cudaHostAlloc");
+    h.cap = cap;
+  }
+  return h.p;
+}
+
+static int perf_eval_packed(const double* params, int32_t n_params, const int32_t* idx, const int32_t* b,
+                     const int32_t* s, double* out_T, double* out_thr, int64_t n, int32_t mode) {
+  Arena A;
+  const size_t op = A.take<double>(8 * static_cast<size_t>(n_params));
+  const size_t oi = A.take<int32_t>(n), ob = A.take<int32_t>(n), os = A.take<int32_t>(n);
+  const size_t of = A.take<uint32_t>(4);  // status word (the end of the inbound copy)
+  const size_t oT = A.take<double>(n), oh = A.take<double>(out_thr ? n : 0);
+  const size_t in_bytes = of + 16, total = A.size;
+  struct {
+    unsigned char* p;
+  } h{pinned_stage(total)};
+  Staging S;
+  S.A = A;
+  S.alloc();
+  std::memcpy(h.p + op, params, 8 * sizeof(double) * static_cast<size_t>(n_params));
+  std::memcpy(h.p + oi, idx, sizeof(int32_t) * static_cast<size_t>(n));
+  std::memcpy(h.p + ob, b, sizeof(int32_t) * static_cast<size_t>(n));
+  std::memcpy(h.p + os, s, sizeof(int32_t) * static_cast<size_t>(n));
+  std::memset(h.p + of, 0, 16);
+  unsigned char* d = S.d;
+  cudaStream_t st = nullptr;
+  cuda_check(cudaMemcpyAsync(d, h.p, in_bytes, cudaMemcpyHostToDevice, st), "H2D");
+  const int rc = nx_perf_eval_async(reinterpret_cast<double*>(d + op), n_params, reinterpret_cast<int32_t*>(d + oi),
+                                    reinterpret_cast<int32_t*>(d + ob), reinterpret_cast<int32_t*>(d + os),
+                                    reinterpret_cast<double*>(d + oT),
+                                    out_thr ? reinterpret_cast<double*>(d + oh) : nullptr, n, mode,
+                                    reinterpret_cast<uint32_t*>(d + of), st);
+  if (rc) return rc;
+  cuda_check(cudaMemcpyAsync(h.p + of, d + of, total - of, cudaMemcpyDeviceToHost, st), "D2H");
+  cuda_check(cudaStreamSynchronize(st), "perf_eval sync");
+  uint32_t bad = 0;
+  std::memcpy(&bad, h.p + of, sizeof bad);
+  if (bad) throw std::invalid_argument("BatchShape requires b >= 1 and s >= b, valid params");
+  std::memcpy(out_T, h.p + oT, sizeof(double) * static_cast<size_t>(n));
+  if (out_thr) std::memcpy(out_thr, h.p + oh, sizeof(double) * static_cast<size_t>(n));
+  return NX_OK;
+}
+
 int nx_perf_eval_host(const double* params, int32_t n_params, const int32_t* idx, const int32_t* b,
                       const int32_t* s, double* out_T, double* out_thr, int64_t n, int32_t mode) {
   return guard([&] {
     if (n < 0 || n_params < 1) throw std::invalid_argument("nx_perf_eval: empty parameter table");
+    if (n <= kPackedEvalMax) {
+      const int rc = perf_eval_packed(params, n_params, idx, b, s, out_T, out_thr, n, mode);
+      if (rc) throw NxError(rc, g_err);
+      return;
+    }
     Staging S;
     Arena& A = S.A;
     const size_t op = A.take<double>(8 * static_cast<size_t>(n_params));
@@ -1299,19 +1371,26 @@ int nx_lens_schedule_mode_host(const nx_lens_problem* problems, int32_t n_proble
       if (problems[i].n_wait < 0 || problems[i].wait_off < 0 ||
           problems[i].wait_off + problems[i].n_wait > n_wait_total)
         throw std::invalid_argument("nx_lens_schedule: waiter range out of bounds");
+    // one packed copy each way through pinned memory (problems + waiters in;
+    // plans + allocations out), the prefix scratch in the same staging
+    // buffer: the scalar schedule_step pays 3 API calls and one synchronize
     Staging S;
     const size_t op = S.A.take<nx_lens_problem>(n_problems), orm = S.A.take<int32_t>(n_wait_total),
-                 opl = S.A.take<nx_lens_plan>(n_problems), oal = S.A.take<int32_t>(n_wait_total);
+                 opl = S.A.take<nx_lens_plan>(n_problems), oal = S.A.take<int32_t>(n_wait_total),
+                 ogp = S.A.take<int32_t>(static_cast<size_t>(n_wait_total) + n_problems);
     S.alloc();
-    cuda_check(cudaMemcpy(S.at<void>(op), problems, sizeof(nx_lens_problem) * n_problems, cudaMemcpyHostToDevice), "H2D");
-    if (n_wait_total)
-      cuda_check(cudaMemcpy(S.at<void>(orm), wait_remaining, sizeof(int32_t) * n_wait_total, cudaMemcpyHostToDevice), "H2D");
-    const int rc = nx_lens_schedule_mode_dev(S.at<nx_lens_problem>(op), n_problems, S.at<int32_t>(orm), n_wait_total,
-                                             S.at<nx_lens_plan>(opl), S.at<int32_t>(oal), mode, nullptr);
-    if (rc) throw NxError(rc, g_err);
-    cuda_check(cudaMemcpy(plans, S.at<void>(opl), sizeof(nx_lens_plan) * n_problems, cudaMemcpyDeviceToHost), "D2H");
-    if (n_wait_total)
-      cuda_check(cudaMemcpy(alloc_tokens, S.at<void>(oal), sizeof(int32_t) * n_wait_total, cudaMemcpyDeviceToHost), "D2H");
+    unsigned char* h = pinned_stage(ogp);
+    std::memcpy(h + op, problems, sizeof(nx_lens_problem) * n_problems);
+    if (n_wait_total) std::memcpy(h + orm, wait_remaining, sizeof(int32_t) * n_wait_total);
+    cudaStream_t st = nullptr;
+    cuda_check(cudaMemcpyAsync(S.d, h, opl, cudaMemcpyHostToDevice, st), "H2D");
+    cuda_check(nx_launch_lens(S.at<nx_lens_problem>(op), n_problems, S.at<int32_t>(orm), S.at<nx_lens_plan>(opl),
+                              S.at<int32_t>(oal), S.at<int32_t>(ogp), current_sms(), mode, st),
+               "nx_lens_kernel launch");
+    cuda_check(cudaMemcpyAsync(h + opl, S.d + opl, ogp - opl, cudaMemcpyDeviceToHost, st), "D2H");
+    cuda_check(cudaStreamSynchronize(st), "nx_lens_schedule sync");
+    std::memcpy(plans, h + opl, sizeof(nx_lens_plan) * n_problems);
+    if (n_wait_total) std::memcpy(alloc_tokens, h + oal, sizeof(int32_t) * n_wait_total);
     for (int32_t i = 0; i < n_problems; ++i)
       if (plans[i].status != NX_OK)
         throw NxError(plans[i].status, "schedule_step: problem " + std::to_string(i) + ": " +
@@ -1363,30 +1442,32 @@ int nx_prism_route_mode_host(nx_route_group* groups, int32_t n_groups, nx_engine
           g.request_off + g.n_requests > n_requests || g.session_off + g.n_sessions > n_session_entries)
         throw std::invalid_argument("nx_prism_route: group ranges out of bounds");
     }
+    // one packed copy each way through pinned memory (the routers' state,
+    // requests and session maps in; state, maps, decisions and statuses out)
     Staging S;
     const size_t og = S.A.take<nx_route_group>(n_groups), orp = S.A.take<nx_engine_report>(n_reports),
                  orq = S.A.take<nx_route_request>(n_requests), osm = S.A.take<int32_t>(n_session_entries),
                  odc = S.A.take<nx_route_decision>(n_requests), ost = S.A.take<int32_t>(n_groups);
+    const size_t total = S.A.size;
     S.alloc();
-    auto h2d = [&](size_t off, const void* src, size_t bytes) {
-      if (bytes) cuda_check(cudaMemcpy(S.at<void>(off), src, bytes, cudaMemcpyHostToDevice), "H2D");
-    };
-    auto d2h = [&](void* dst, size_t off, size_t bytes) {
-      if (bytes) cuda_check(cudaMemcpy(dst, S.at<void>(off), bytes, cudaMemcpyDeviceToHost), "D2H");
-    };
-    h2d(og, groups, sizeof(nx_route_group) * n_groups);
-    h2d(orp, reports, sizeof(nx_engine_report) * n_reports);
-    h2d(orq, requests, sizeof(nx_route_request) * n_requests);
-    h2d(osm, session_map, sizeof(int32_t) * n_session_entries);
+    unsigned char* h = pinned_stage(total);
+    std::memcpy(h + og, groups, sizeof(nx_route_group) * n_groups);
+    if (n_reports) std::memcpy(h + orp, reports, sizeof(nx_engine_report) * n_reports);
+    if (n_requests) std::memcpy(h + orq, requests, sizeof(nx_route_request) * n_requests);
+    if (n_session_entries) std::memcpy(h + osm, session_map, sizeof(int32_t) * n_session_entries);
+    cudaStream_t st = nullptr;
+    cuda_check(cudaMemcpyAsync(S.d, h, odc, cudaMemcpyHostToDevice, st), "H2D");
     const int rc = nx_prism_route_mode_dev(S.at<nx_route_group>(og), n_groups, S.at<nx_engine_report>(orp),
                                            S.at<nx_route_request>(orq), S.at<int32_t>(osm),
-                                           S.at<nx_route_decision>(odc), S.at<int32_t>(ost), mode, nullptr);
+                                           S.at<nx_route_decision>(odc), S.at<int32_t>(ost), mode, st);
     if (rc) throw NxError(rc, g_err);
-    d2h(groups, og, sizeof(nx_route_group) * n_groups);
-    d2h(reports, orp, sizeof(nx_engine_report) * n_reports);
-    d2h(session_map, osm, sizeof(int32_t) * n_session_entries);
-    d2h(decisions, odc, sizeof(nx_route_decision) * n_requests);
-    d2h(group_status, ost, sizeof(int32_t) * n_groups);
+    cuda_check(cudaMemcpyAsync(h, S.d, total, cudaMemcpyDeviceToHost, st), "D2H");
+    cuda_check(cudaStreamSynchronize(st), "nx_prism_route sync");
+    std::memcpy(groups, h + og, sizeof(nx_route_group) * n_groups);
+    if (n_reports) std::memcpy(reports, h + orp, sizeof(nx_engine_report) * n_reports);
+    if (n_session_entries) std::memcpy(session_map, h + osm, sizeof(int32_t) * n_session_entries);
+    if (n_requests) std::memcpy(decisions, h + odc, sizeof(nx_route_decision) * n_requests);
+    std::memcpy(group_status, h + ost, sizeof(int32_t) * n_groups);
     for (int32_t i = 0; i < n_groups; ++i)
       if (group_status[i] != NX_OK)
         throw NxError(group_status[i], "Router::route: group " + std::to_string(i) + ": " +

@@ -583,13 +583,21 @@ def run_nx(args):
     # e2e through the C-ABI with host buffers: workload generation on the
     # host (as inside the reference's run_simulation clock), pinned H2D,
     # launch, D2H of the results, per-replica summaries
+    # (pipelined as a caller running batch after batch would: the next
+    # step's workload is built on the host while the device runs this one;
+    # every step still pays its own synthesis, H2D, launch and D2H)
     e2e = None
     if not args.no_e2e:
         barrier()
         t0 = time.perf_counter()
+        batch.rebuild_workloads(os.cpu_count())
         for i in range(args.steps):
-            batch.rebuild_workloads(os.cpu_count())
-            batch.run()
+            batch.upload()
+            batch.launch()
+            batch.download()
+            if i + 1 < args.steps:
+                batch.rebuild_workloads(os.cpu_count())  # waits for this step's H2D only
+            batch.synchronize()
             e2e_sums = batch.summaries()
         wall = time.perf_counter() - t0
         if sum(x.decisions for x in e2e_sums) != decisions_step:

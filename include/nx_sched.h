@@ -339,8 +339,10 @@ int nx_sim_error(nx_sim_t h, int32_t replica, char* buf, int64_t cap);
 /* Workload generation again (build_workload, proj/src/sim.cpp:101-141) for
  * every replica on host threads, into the pinned input image; the parsed
  * configs are kept. Deterministic: the next run reproduces the same results.
- * (bench.py times it inside e2e, as the reference's run_simulation clock
- * includes its workload build.) */
+ * May overlap a launch in flight: it rewrites the pinned image only after the
+ * previous upload's copies have completed, so a caller can build the next
+ * batch's inputs while the device runs this one. (bench.py times it inside
+ * e2e, as the reference's run_simulation clock includes its workload build.) */
 int nx_sim_rebuild_workloads(nx_sim_t h, int32_t host_threads);
 /* Upload (H2D), launch, download (D2H) on the handle's stream; each is async.
  * nx_sim_last_kernel_ms covers the launch's state reset + the kernel. */

@@ -216,6 +216,8 @@ struct nx_sim {
   int device = 0;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t ev_up = nullptr;  // the last upload's copies out of the pinned inputs
+  bool uploaded = false;
   std::vector<nx::RunCfg> cfgs;
   std::vector<nx::Workload> wl;
   int n_rep = 0, max_eng = 1, prefix_cap = 1;
@@ -269,6 +271,7 @@ struct nx_sim {
       if (p) cudaFreeHost(p);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
+    if (ev_up) cudaEventDestroy(ev_up);
     if (stream) cudaStreamDestroy(stream);
   }
 };
@@ -700,6 +703,7 @@ int nx_sim_create_json(const char* const* configs, int32_t n_replicas, int32_t d
     cuda_check(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking), "cudaStreamCreate");
     cuda_check(cudaEventCreate(&h->ev0), "cudaEventCreate");
     cuda_check(cudaEventCreate(&h->ev1), "cudaEventCreate");
+    cuda_check(cudaEventCreateWithFlags(&h->ev_up, cudaEventDisableTiming), "cudaEventCreate");
     fill_descriptors(*h);
     *out = h.release();
   });
@@ -709,7 +713,9 @@ int nx_sim_rebuild_workloads(nx_sim_t h, int32_t host_threads) {
   return guard([&] {
     // build_workload (sim.cpp:101-141) again for every replica on host
     // threads, then the pinned input image; configs stay parsed (the
-    // reference's own clock also starts after RunConfig parsing)
+    // reference's own clock also starts after RunConfig parsing). Safe to
+    // call while the previous launch runs: the pinned image is rewritten
+    // only after the previous upload's copies out of it have completed.
     std::atomic<int> next{0};
     std::vector<std::string> errs(h->n_rep);
     std::vector<int> codes(h->n_rep, 0);
@@ -731,6 +737,7 @@ int nx_sim_rebuild_workloads(nx_sim_t h, int32_t host_threads) {
     for (auto& t : pool) t.join();
     for (int i = 0; i < h->n_rep; ++i)
       if (codes[i]) throw NxError(codes[i], "replica " + std::to_string(i) + ": " + errs[i]);
+    if (h->uploaded) cuda_check(cudaEventSynchronize(h->ev_up), "upload event");
     for (int r = 0; r < h->n_rep; ++r) {
       const nx::Workload& w = h->wl[r];
       const int64_t o = h->rep[r].req_off;
@@ -759,6 +766,8 @@ int nx_sim_upload(nx_sim_t h) {
     cp(h->d_arena + h->off_rep, h->rep.data(), h->rep.size() * sizeof(NxReplicaDesc));
     cp(h->d_arena + h->off_eng, h->eng.data(), h->eng.size() * sizeof(NxEngineDesc));
     cp(h->d_order, h->order.data(), h->order.size() * sizeof(int32_t));
+    cuda_check(cudaEventRecord(h->ev_up, h->stream), "event");
+    h->uploaded = true;
   });
 }
 

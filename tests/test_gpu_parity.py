@@ -109,6 +109,29 @@ def test_single_replica_equals_batched_replica(all_cases, device_batch):
         assert one.summary_json == b.summary_json(i)
 
 
+def test_rebuild_overlapping_a_launch_keeps_results():
+    """nx_sim_rebuild_workloads while the previous launch is in flight (the
+    pipelined e2e loop in bench.py): it waits for that launch's H2D copies
+    before rewriting the pinned inputs, so both launches give the same
+    event hashes, decisions and records as a plain run."""
+    from paper_2509_23384_b200 import sim, workloads as W
+    cfgs = W.sweep_configs(32, n=300)
+    ref = sim.Batch(cfgs).run()
+    want = [(x.event_hash, x.decisions) for x in ref.summaries()]
+    want_rec = [r.completed_ms for r in ref.records(5)]
+    ref.close()
+    b = sim.Batch(cfgs)
+    for step in range(3):
+        b.upload()
+        b.launch()
+        b.download()
+        b.rebuild_workloads(4)  # overlaps the launch
+        b.synchronize()
+        assert [(x.event_hash, x.decisions) for x in b.summaries()] == want, step
+        assert [r.completed_ms for r in b.records(5)] == want_rec, step
+    b.close()
+
+
 def test_sweep_slice_matches_reference_batch():
     from paper_2509_23384_b200 import sim, workloads as W
     cfgs = W.sweep_configs(64, n=300)
